@@ -1,0 +1,235 @@
+// Kernel-task DAG of a tiled QR elimination list, its discrete-event critical
+// path, and the strip-refined device task graphs (product code; independent of
+// oracle/).
+//
+// Expansion (§2.1): TT family = Algorithm 3 (lines 289-307), TS
+// family = Algorithm 2 (lines 254-268); "if a tile is already in triangle form,
+// then the associated GEQRT and update kernels are not applied" (lines 333-335);
+// a TS elimination of a tile that already is a triangle (it was a pivot earlier
+// in the column) uses TTQRT/TTMQR (reading R6); finally every
+// diagonal tile not yet a triangle is factored by GEQRT (the square case of
+// Theorem 1(1)).
+// Dependencies (execution scheme §2.3, with the NODEP relaxation
+// of §4): successive writers of a tile are chained; an update
+// waits for the panel kernel whose reflectors it applies; reading reflectors
+// does not block a later writer (the reflectors and the rewritten part of the
+// tile are disjoint).
+#include <algorithm>
+#include <numeric>
+#include "plan.h"
+
+namespace tqr {
+
+void expand(const std::vector<Elim> &lst, int p, int q, int family, std::vector<TileTask> &tasks) {
+  tasks.clear();
+  const int kmax = std::min(p, q);
+  std::vector<int> last((size_t)(p + 1) * (q + 1), -1);   // last writer per tile (1-based)
+  std::vector<char> tri((size_t)(p + 1) * (q + 1), 0);
+  std::vector<int> geqrt_of((size_t)(p + 1) * (q + 1), -1);
+  auto at = [q](int r, int c) { return (size_t)r * (q + 1) + c; };
+
+  auto emit = [&](int kind, int i, int piv, int k, int j, int reads, std::initializer_list<std::pair<int, int>> writes) {
+    TileTask t{kind, i, piv, k, j, {}};
+    if (reads >= 0) t.deps.push_back(reads);
+    for (auto &w : writes) {
+      int lw = last[at(w.first, w.second)];
+      if (lw >= 0) t.deps.push_back(lw);
+    }
+    std::sort(t.deps.begin(), t.deps.end());
+    t.deps.erase(std::unique(t.deps.begin(), t.deps.end()), t.deps.end());
+    int id = (int)tasks.size();
+    for (auto &w : writes) last[at(w.first, w.second)] = id;
+    tasks.push_back(std::move(t));
+    return id;
+  };
+  auto factor = [&](int r, int k) {
+    int g = emit(K_GEQRT, r, 0, k, 0, -1, {{r, k}});
+    geqrt_of[at(r, k)] = g;
+    for (int j = k + 1; j <= q; ++j) emit(K_UNMQR, r, 0, k, j, g, {{r, j}});
+    tri[at(r, k)] = 1;
+  };
+  for (const Elim &e : lst) {
+    const int i = e.i, pv = e.piv, k = e.k;
+    if (!tri[at(pv, k)]) factor(pv, k);
+    int qrt, mqr;
+    if (family == 0 || tri[at(i, k)]) {
+      if (!tri[at(i, k)]) factor(i, k);
+      qrt = K_TTQRT; mqr = K_TTMQR;
+    } else {
+      qrt = K_TSQRT; mqr = K_TSMQR;
+    }
+    int x = emit(qrt, i, pv, k, 0, -1, {{pv, k}, {i, k}});
+    for (int j = k + 1; j <= q; ++j) emit(mqr, i, pv, k, j, x, {{pv, j}, {i, j}});
+  }
+  for (int k = 1; k <= kmax; ++k)
+    if (!tri[at(k, k)]) factor(k, k);
+}
+
+int64_t simulate(const std::vector<TileTask> &tasks, std::vector<int64_t> &start,
+                 std::vector<int64_t> &finish) {
+  start.assign(tasks.size(), 0);
+  finish.assign(tasks.size(), 0);
+  int64_t mk = 0;
+  for (size_t t = 0; t < tasks.size(); ++t) {
+    int64_t s = 0;
+    for (int d : tasks[t].deps) s = std::max(s, finish[d]);
+    start[t] = s;
+    finish[t] = s + kind_weight(tasks[t].kind);
+    mk = std::max(mk, finish[t]);
+  }
+  return mk;
+}
+
+namespace {
+
+// Reorder a graph built in a topological emission order by a priority key
+// that is itself topological (key(dep) < key(task)), then remap dependencies.
+void reorder(DevGraph &g, const std::vector<std::pair<int64_t, int64_t>> &key,
+             const std::vector<std::vector<int>> &deps) {
+  const int n = (int)g.tasks.size();
+  std::vector<int> ord(n);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return key[a] < key[b]; });
+  std::vector<int> pos(n);
+  for (int r = 0; r < n; ++r) pos[ord[r]] = r;
+  std::vector<DevTask> out(n);
+  g.deps.clear();
+  for (int r = 0; r < n; ++r) {
+    DevTask t = g.tasks[ord[r]];
+    t.dep_begin = (int32_t)g.deps.size();
+    for (int d : deps[ord[r]]) g.deps.push_back(pos[d]);
+    t.dep_end = (int32_t)g.deps.size();
+    out[r] = t;
+  }
+  g.tasks.swap(out);
+}
+
+DevTask mk(int kind, int i, int piv, int k, int j, int s) {
+  DevTask t;
+  t.kind = (int16_t)kind; t.i = (int16_t)i; t.piv = (int16_t)piv; t.k = (int16_t)k;
+  t.j = (int16_t)j; t.s = (int16_t)s; t.dep_begin = t.dep_end = 0; t.pad = 0;
+  return t;
+}
+
+}  // namespace
+
+void build_factor_graph(const std::vector<TileTask> &tt, const std::vector<int64_t> &start,
+                        int p, int q, int nb, int ws, DevGraph &g) {
+  const int S = (nb + ws - 1) / ws;
+  g.tasks.clear();
+  std::vector<std::vector<int>> deps;
+  std::vector<std::pair<int64_t, int64_t>> key;
+  // last device writer of every (tile, strip); tiles 0-based
+  std::vector<int> lw((size_t)p * q * S, -1);
+  auto slot = [p, S](int r, int c, int s) { return ((size_t)c * p + r) * S + s; };
+  std::vector<int> panel_dev(tt.size(), -1);
+  std::vector<int> dl;
+  auto add = [&](DevTask t, std::vector<int> &d, int64_t prio) {
+    std::sort(d.begin(), d.end());
+    d.erase(std::unique(d.begin(), d.end()), d.end());
+    g.tasks.push_back(t);
+    deps.push_back(d);
+    key.emplace_back(prio, (int64_t)g.tasks.size());
+    return (int)g.tasks.size() - 1;
+  };
+  for (size_t x = 0; x < tt.size(); ++x) {
+    const TileTask &t = tt[x];
+    const int i = t.i - 1, pv = t.piv - 1, k = t.k - 1, j = t.j - 1;
+    switch (t.kind) {
+      case K_GEQRT: {
+        dl.clear();
+        for (int s = 0; s < S; ++s) if (lw[slot(i, k, s)] >= 0) dl.push_back(lw[slot(i, k, s)]);
+        int id = add(mk(K_GEQRT, i, 0, k, 0, 0), dl, start[x]);
+        for (int s = 0; s < S; ++s) lw[slot(i, k, s)] = id;
+        panel_dev[x] = id;
+        break;
+      }
+      case K_TTQRT: case K_TSQRT: {
+        dl.clear();
+        for (int s = 0; s < S; ++s) {
+          if (lw[slot(pv, k, s)] >= 0) dl.push_back(lw[slot(pv, k, s)]);
+          if (lw[slot(i, k, s)] >= 0) dl.push_back(lw[slot(i, k, s)]);
+        }
+        int id = add(mk(t.kind, i, pv, k, 0, 0), dl, start[x]);
+        for (int s = 0; s < S; ++s) lw[slot(pv, k, s)] = lw[slot(i, k, s)] = id;
+        panel_dev[x] = id;
+        break;
+      }
+      case K_UNMQR: {
+        // the reflector source is the GEQRT of tile (i,k): the unique dep with kind GEQRT on (i,k)
+        int src = -1;
+        for (int d : t.deps)
+          if (tt[d].kind == K_GEQRT && tt[d].i == t.i && tt[d].k == t.k) src = panel_dev[d];
+        for (int s = 0; s < S; ++s) {
+          dl.clear();
+          dl.push_back(src);
+          if (lw[slot(i, j, s)] >= 0) dl.push_back(lw[slot(i, j, s)]);
+          int id = add(mk(K_UNMQR, i, 0, k, j, s), dl, start[x]);
+          lw[slot(i, j, s)] = id;
+        }
+        break;
+      }
+      case K_TTMQR: case K_TSMQR: {
+        int src = -1;
+        const int qk = t.kind == K_TTMQR ? K_TTQRT : K_TSQRT;
+        for (int d : t.deps)
+          if (tt[d].kind == qk && tt[d].i == t.i && tt[d].k == t.k) src = panel_dev[d];
+        for (int s = 0; s < S; ++s) {
+          dl.clear();
+          dl.push_back(src);
+          if (lw[slot(pv, j, s)] >= 0) dl.push_back(lw[slot(pv, j, s)]);
+          if (lw[slot(i, j, s)] >= 0) dl.push_back(lw[slot(i, j, s)]);
+          int id = add(mk(t.kind, i, pv, k, j, s), dl, start[x]);
+          lw[slot(pv, j, s)] = lw[slot(i, j, s)] = id;
+        }
+        break;
+      }
+      default: break;
+    }
+  }
+  reorder(g, key, deps);
+}
+
+void build_apply_graph(const std::vector<TileTask> &tt, int p, int qc, int nb, int ws,
+                       bool trans, DevGraph &g) {
+  const int S = (nb + ws - 1) / ws;
+  g.tasks.clear();
+  std::vector<std::vector<int>> deps;
+  std::vector<std::pair<int64_t, int64_t>> key;
+  std::vector<int> lw((size_t)p * qc * S, -1);
+  std::vector<int64_t> fin;   // ASAP finish of each device task (priority)
+  auto slot = [p, S](int r, int c, int s) { return ((size_t)c * p + r) * S + s; };
+  std::vector<size_t> order;
+  for (size_t x = 0; x < tt.size(); ++x)
+    if (tt[x].kind == K_GEQRT || tt[x].kind == K_TTQRT || tt[x].kind == K_TSQRT) order.push_back(x);
+  if (!trans) std::reverse(order.begin(), order.end());
+  for (size_t x : order) {
+    const TileTask &t = tt[x];
+    const int i = t.i - 1, pv = t.piv - 1, k = t.k - 1;
+    for (int c = 0; c < qc; ++c)
+      for (int s = 0; s < S; ++s) {
+        std::vector<int> d;
+        int64_t st = 0;
+        int kind, w;
+        if (t.kind == K_GEQRT) {
+          kind = K_AP_UNMQR; w = 6;
+          if (lw[slot(i, c, s)] >= 0) d.push_back(lw[slot(i, c, s)]);
+        } else {
+          kind = t.kind == K_TTQRT ? K_AP_TTMQR : K_AP_TSMQR; w = t.kind == K_TTQRT ? 6 : 12;
+          if (lw[slot(pv, c, s)] >= 0) d.push_back(lw[slot(pv, c, s)]);
+          if (lw[slot(i, c, s)] >= 0) d.push_back(lw[slot(i, c, s)]);
+        }
+        for (int y : d) st = std::max(st, fin[y]);
+        g.tasks.push_back(mk(kind, i, t.kind == K_GEQRT ? 0 : pv, k, c, s));
+        deps.push_back(d);
+        fin.push_back(st + w);
+        key.emplace_back(st, (int64_t)g.tasks.size());
+        int id = (int)g.tasks.size() - 1;
+        lw[slot(i, c, s)] = id;
+        if (t.kind != K_GEQRT) lw[slot(pv, c, s)] = id;
+      }
+  }
+  reorder(g, key, deps);
+}
+
+}  // namespace tqr

@@ -1,0 +1,282 @@
+// B200 (sm_100a) tiled QR: one persistent dataflow kernel executes the whole
+// task graph of an elimination list (§2.3 execution scheme, lines
+// 385-411), with the six tile kernels of Table 1 (lines 239-251) as device
+// routines. See DESIGN.md §5 for the design and include/tiledqr.h for the ABI.
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "plan.h"
+#include "tqr_device.cuh"
+#include "../../include/tiledqr.h"
+
+using namespace tqr;
+
+// ============================================================================
+// Host side: errors, plans, launches
+// ============================================================================
+static thread_local std::string g_err;
+static thread_local int g_launches = 0;
+
+static int fail(int code, const std::string &msg) { g_err = msg; return code; }
+static int cuda_fail(cudaError_t e, const char *where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return TQR_ECUDA;
+}
+#define CUDA_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) return cuda_fail(_e, #x); } while (0)
+
+extern "C" const char *tqr_last_error(void) { return g_err.c_str(); }
+extern "C" int tqr_version(void) { return 100; }
+extern "C" int tqr_last_launch_count(void) { return g_launches; }
+
+extern "C" int elim_list(int p, int q, int tree, int bs, int32_t *i, int32_t *piv, int32_t *k,
+                         int32_t *step, int64_t cap) {
+  std::vector<Elim> lst;
+  std::string err;
+  if (!build_elim_list(p, q, tree, bs, lst, err)) return fail(TQR_EINVAL, err);
+  if ((int64_t)lst.size() > cap) return fail(TQR_ECAP, "elim_list: capacity too small");
+  if (!lst.empty() && (!i || !piv || !k)) return fail(TQR_EINVAL, "elim_list: null output");
+  for (size_t x = 0; x < lst.size(); ++x) {
+    i[x] = lst[x].i; piv[x] = lst[x].piv; k[x] = lst[x].k;
+    if (step) step[x] = lst[x].step;
+  }
+  return (int)lst.size();
+}
+
+static int tile_sim(int p, int q, int tree, int bs, int family, std::vector<TileTask> &tt,
+                    std::vector<int64_t> &st, std::vector<int64_t> &fin, int64_t &mk) {
+  std::vector<Elim> lst;
+  std::string err;
+  if (family != TQR_TT && family != TQR_TS) return fail(TQR_EINVAL, "unknown kernel family");
+  if (!build_elim_list(p, q, tree, bs, lst, err)) return fail(TQR_EINVAL, err);
+  expand(lst, p, q, family, tt);
+  mk = simulate(tt, st, fin);
+  return 0;
+}
+
+extern "C" int64_t critical_path(int p, int q, int tree, int bs, int family) {
+  std::vector<TileTask> tt;
+  std::vector<int64_t> st, fin;
+  int64_t mk;
+  int rc = tile_sim(p, q, tree, bs, family, tt, st, fin, mk);
+  return rc < 0 ? rc : mk;
+}
+
+extern "C" int64_t tiled_times(int p, int q, int tree, int bs, int family, int32_t *zt) {
+  std::vector<TileTask> tt;
+  std::vector<int64_t> st, fin;
+  int64_t mk;
+  int rc = tile_sim(p, q, tree, bs, family, tt, st, fin, mk);
+  if (rc < 0) return rc;
+  if (!zt) return fail(TQR_EINVAL, "tiled_times: null output");
+  for (int x = 0; x < p * q; ++x) zt[x] = 0;
+  for (size_t x = 0; x < tt.size(); ++x)
+    if (tt[x].kind == K_TTQRT || tt[x].kind == K_TSQRT)
+      zt[(tt[x].k - 1) * p + (tt[x].i - 1)] = (int32_t)fin[x];
+  return mk;
+}
+
+// ---- strip width and shared-memory footprint --------------------------------
+static int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+static int pick_ws(int nb, int ib) {
+  int forced = env_int("TQR_WS", 0);
+  if (forced > 0) return forced < nb ? forced : nb;
+  if (nb <= 8) return nb;
+  static const int cand[] = {64, 56, 48, 40, 32, 24, 16, 8};
+  for (int w : cand)
+    if (w <= nb && nb % w == 0 && smem_bytes(nb, ib, w) <= kMaxSmem) return w;
+  for (int w : cand)
+    if (w <= nb && smem_bytes(nb, ib, w) <= kMaxSmem) return w;
+  return 8;
+}
+
+// ---- plan cache -------------------------------------------------------------
+struct DevPlan {
+  DevTask *tasks = nullptr;
+  int32_t *deps = nullptr;
+  int *done = nullptr;      // per-task completion epoch
+  int *ctrl = nullptr;      // [0] = next task, [1] = CTAs exited
+  int ntask = 0;
+  int epoch = 0;
+  int ws = 0;
+  ~DevPlan() {
+    cudaFree(tasks); cudaFree(deps); cudaFree(done); cudaFree(ctrl);
+  }
+};
+
+using PlanKey = std::tuple<int, int, int, int, int, int, int, int, int, int, int>;
+static std::mutex g_mu;
+static std::map<PlanKey, std::unique_ptr<DevPlan>> g_plans;
+
+static int upload(const DevGraph &g, int ws, DevPlan &pl) {
+  pl.ntask = (int)g.tasks.size();
+  pl.ws = ws;
+  size_t tb = sizeof(DevTask) * (g.tasks.size() ? g.tasks.size() : 1);
+  size_t db = sizeof(int32_t) * (g.deps.size() ? g.deps.size() : 1);
+  CUDA_TRY(cudaMalloc(&pl.tasks, tb));
+  CUDA_TRY(cudaMalloc(&pl.deps, db));
+  CUDA_TRY(cudaMalloc(&pl.done, sizeof(int) * (pl.ntask ? pl.ntask : 1)));
+  CUDA_TRY(cudaMalloc(&pl.ctrl, sizeof(int) * 4));
+  if (!g.tasks.empty()) CUDA_TRY(cudaMemcpy(pl.tasks, g.tasks.data(), sizeof(DevTask) * g.tasks.size(), cudaMemcpyHostToDevice));
+  if (!g.deps.empty()) CUDA_TRY(cudaMemcpy(pl.deps, g.deps.data(), sizeof(int32_t) * g.deps.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemset(pl.done, 0, sizeof(int) * (pl.ntask ? pl.ntask : 1)));
+  CUDA_TRY(cudaMemset(pl.ctrl, 0, sizeof(int) * 4));
+  return 0;
+}
+
+// mode: 0 factor, 1 apply Q^T, 2 apply Q
+static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, int bs, int family,
+                    DevPlan **out) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  int ws = pick_ws(nb, ib);
+  PlanKey key{dev, mode, p, q, qc, nb, ib, tree, bs, family, ws};
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_plans.find(key);
+  if (it != g_plans.end()) { *out = it->second.get(); return 0; }
+  std::vector<TileTask> tt;
+  std::vector<int64_t> st, fin;
+  int64_t mk;
+  int rc = tile_sim(p, q, tree, bs, family, tt, st, fin, mk);
+  if (rc < 0) return rc;
+  DevGraph g;
+  if (mode == 0) build_factor_graph(tt, st, p, q, nb, ws, g);
+  else build_apply_graph(tt, p, qc, nb, ws, mode == 1, g);
+  auto pl = std::make_unique<DevPlan>();
+  rc = upload(g, ws, *pl);
+  if (rc < 0) return rc;
+  *out = pl.get();
+  g_plans[key] = std::move(pl);
+  return 0;
+}
+
+extern "C" void tqr_release_plans(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_plans.clear();
+}
+
+static int check_shape(int m, int n, int nb, int ib, int &p, int &q) {
+  if (nb < 1 || ib < 1 || m < 1 || n < 1) return fail(TQR_EINVAL, "need m, n, nb, ib >= 1");
+  if (nb > kMaxNb) return fail(TQR_EUNSUP, "nb > 256 is not supported");
+  if (ib > kMaxIb) return fail(TQR_EUNSUP, "ib > 32 is not supported");
+  if (m % nb || n % nb) return fail(TQR_EINVAL, "nb must divide m and n");
+  p = m / nb; q = n / nb;
+  if (q > p) return fail(TQR_EINVAL, "need m >= n");
+  if (p > 32767 || q > 32767) return fail(TQR_EUNSUP, "too many tiles");
+  return 0;
+}
+
+static int launch(DevPlan *pl, int p, int q, int nb, int ib, double *A, double *T, double *C,
+                  int trans, cudaStream_t stream) {
+  if (pl->ntask == 0) { g_launches = 0; return 0; }
+  int dev = 0, sms = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  size_t smem = smem_bytes(nb, ib, pl->ws);
+  static thread_local int attr_set_dev = -1;
+  if (attr_set_dev != dev) {
+    int optin = 0;
+    cudaFuncAttributes fa;
+    CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    CUDA_TRY(cudaFuncGetAttributes(&fa, tqr_persistent));
+    CUDA_TRY(cudaFuncSetAttribute(tqr_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  optin - (int)fa.sharedSizeBytes));
+    attr_set_dev = dev;
+  }
+  RunArgs a;
+  a.tasks = pl->tasks; a.deps = pl->deps; a.ntask = pl->ntask;
+  a.done = pl->done; a.ctrl = pl->ctrl; a.epoch = ++pl->epoch;
+  a.A = A; a.T = T; a.C = C;
+  a.p = p; a.q = q; a.nb = nb; a.ib = ib; a.ws = pl->ws; a.trans = trans;
+  int grid = sms;
+  int forced = env_int("TQR_GRID", 0);
+  if (forced > 0) grid = forced;
+  if (grid > pl->ntask) grid = pl->ntask;
+  a.nctas = grid;
+  tqr_persistent<<<grid, kThreads, smem, stream>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  g_launches = 1;
+  return 0;
+}
+
+extern "C" int tiled_qr(int m, int n, int nb, int ib, int tree, int bs, int family, double *A,
+                        double *T, void *stream) {
+  int p, q;
+  int rc = check_shape(m, n, nb, ib, p, q);
+  if (rc < 0) return rc;
+  if (!A || !T) return fail(TQR_EINVAL, "tiled_qr: null pointer");
+  DevPlan *pl;
+  rc = get_plan(0, p, q, 0, nb, ib, tree, bs, family, &pl);
+  if (rc < 0) return rc;
+  return launch(pl, p, q, nb, ib, A, T, nullptr, 1, (cudaStream_t)stream);
+}
+
+static int apply_common(int trans, int m, int n, int nb, int ib, int tree, int bs, int family,
+                        const double *A, const double *T, double *C, int nrhs, void *stream) {
+  int p, q;
+  int rc = check_shape(m, n, nb, ib, p, q);
+  if (rc < 0) return rc;
+  if (!A || !T || !C) return fail(TQR_EINVAL, "apply: null pointer");
+  if (nrhs < 0 || nrhs % nb) return fail(TQR_EINVAL, "apply: nrhs must be a multiple of nb");
+  int qc = nrhs / nb;
+  if (qc == 0) { g_launches = 0; return 0; }
+  DevPlan *pl;
+  rc = get_plan(trans ? 1 : 2, p, q, qc, nb, ib, tree, bs, family, &pl);
+  if (rc < 0) return rc;
+  return launch(pl, p, q, nb, ib, const_cast<double *>(A), const_cast<double *>(T), C, trans,
+                (cudaStream_t)stream);
+}
+
+extern "C" int apply_qt(int m, int n, int nb, int ib, int tree, int bs, int family,
+                        const double *A, const double *T, double *C, int nrhs, void *stream) {
+  return apply_common(1, m, n, nb, ib, tree, bs, family, A, T, C, nrhs, stream);
+}
+
+extern "C" int apply_q(int m, int n, int nb, int ib, int tree, int bs, int family,
+                       const double *A, const double *T, double *C, int nrhs, void *stream) {
+  return apply_common(0, m, n, nb, ib, tree, bs, family, A, T, C, nrhs, stream);
+}
+
+// ---- end-to-end on host buffers ----------------------------------------------
+struct Scratch { double *A = nullptr, *T = nullptr; size_t na = 0, nt = 0; int dev = -1; };
+static std::mutex g_smu;
+static Scratch g_scratch;
+
+extern "C" int tiled_qr_host(int m, int n, int nb, int ib, int tree, int bs, int family,
+                             double *A_host, double *T_host, void *stream) {
+  int p, q;
+  int rc = check_shape(m, n, nb, ib, p, q);
+  if (rc < 0) return rc;
+  if (!A_host || !T_host) return fail(TQR_EINVAL, "tiled_qr_host: null pointer");
+  std::lock_guard<std::mutex> lk(g_smu);
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  size_t na = (size_t)m * n, nt = (size_t)p * q * 2 * ib * nb;
+  if (g_scratch.dev != dev || g_scratch.na < na || g_scratch.nt < nt) {
+    cudaFree(g_scratch.A); cudaFree(g_scratch.T);
+    g_scratch = Scratch();
+    CUDA_TRY(cudaMalloc(&g_scratch.A, na * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&g_scratch.T, nt * sizeof(double)));
+    g_scratch.na = na; g_scratch.nt = nt; g_scratch.dev = dev;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemcpyAsync(g_scratch.A, A_host, na * sizeof(double), cudaMemcpyHostToDevice, s));
+  rc = tiled_qr(m, n, nb, ib, tree, bs, family, g_scratch.A, g_scratch.T, stream);
+  if (rc < 0) return rc;
+  CUDA_TRY(cudaMemcpyAsync(A_host, g_scratch.A, na * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(T_host, g_scratch.T, nt * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return 0;
+}
