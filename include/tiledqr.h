@@ -140,6 +140,19 @@ int apply_q(int m, int n, int nb, int ib, int tree, int bs, int family,
 int tiled_qr_host(int m, int n, int nb, int ib, int tree, int bs, int family,
                   double *A_host, double *T_host, void *stream);
 
+/* Diagnostics: per-task tracing of the persistent kernel. While enabled, every
+ * launch records, per task, globaltimer stamps (taken, dependencies ready,
+ * done) and the SM id. tqr_trace_fetch copies the last traced launch to
+ * `out` as 16 uint64 per task in execution-priority order: taken, ready, done,
+ * smid, kind (Table 1 kernel: 0 GEQRT, 1 UNMQR, 2 TTQRT, 3 TTMQR, 4 TSQRT,
+ * 5 TSMQR, 6-8 apply kinds), i | piv<<16, k | j<<16 (0-based), strip, then
+ * 8 SM-cycle counters of the task's phases (load wait, V fix-up, V^T C
+ * contraction, T multiply, V W contraction, panel columns, T recurrence,
+ * stores/other). Returns the task count or a negative TQR_E* code
+ * (TQR_ECAP if cap < 16*n). */
+int tqr_trace_enable(int on);
+int64_t tqr_trace_fetch(uint64_t *out, int64_t cap);
+
 /* Number of kernel launches the last device call issued (for bench accounting). */
 int tqr_last_launch_count(void);
 

@@ -38,6 +38,8 @@ _SIGS = {
     "apply_qt": (ctypes.c_int, [ctypes.c_int] * 7 + [_VP, _VP, _VP, ctypes.c_int, _VP]),
     "apply_q": (ctypes.c_int, [ctypes.c_int] * 7 + [_VP, _VP, _VP, ctypes.c_int, _VP]),
     "tiled_qr_host": (ctypes.c_int, [ctypes.c_int] * 7 + [_VP, _VP, _VP]),
+    "tqr_trace_enable": (ctypes.c_int, [ctypes.c_int]),
+    "tqr_trace_fetch": (ctypes.c_int64, [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int64]),
     "tqr_last_launch_count": (ctypes.c_int, []),
     "tqr_release_plans": (None, []),
     "tqr_last_error": (ctypes.c_char_p, []),
@@ -174,6 +176,34 @@ def tiled_qr_host(A_host: np.ndarray, m: int, n: int, nb: int, ib: int = 32, tre
     _check(lib().tiled_qr_host(m, n, nb, ib, _tree(tree), bs, _fam(family), ctypes.c_void_p(A_host.ctypes.data),
                                ctypes.c_void_p(T_host.ctypes.data), s))
     return T_host
+
+
+def trace_enable(on: bool = True):
+    """Diagnostics: record per-task timestamps of subsequent launches."""
+    lib().tqr_trace_enable(1 if on else 0)
+
+
+KIND_NAMES = ["GEQRT", "UNMQR", "TTQRT", "TTMQR", "TSQRT", "TSMQR", "AP_UNMQR", "AP_TTMQR", "AP_TSMQR"]
+
+
+PHASES = ["load", "fix", "mma1", "tri", "mma3", "panel", "trec", "store"]
+
+
+def trace_fetch():
+    """Per-task trace of the last traced launch: structured numpy array."""
+    cap = 16 * 4_000_000
+    buf = np.zeros(cap, np.uint64)
+    n = _check(lib().tqr_trace_fetch(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), cap))
+    r = buf[: 16 * n].reshape(n, 16).astype(np.int64)
+    dt = [("taken", "i8"), ("ready", "i8"), ("done", "i8"), ("sm", "i4"), ("kind", "i4"), ("i", "i4"),
+          ("piv", "i4"), ("k", "i4"), ("j", "i4"), ("s", "i4")] + [(f"c_{p}", "i8") for p in PHASES]
+    out = np.zeros(n, dtype=dt)
+    out["taken"], out["ready"], out["done"], out["sm"], out["kind"] = r[:, 0], r[:, 1], r[:, 2], r[:, 3], r[:, 4]
+    out["i"], out["piv"] = r[:, 5] & 0xFFFF, (r[:, 5] >> 16) & 0xFFFF
+    out["k"], out["j"], out["s"] = r[:, 6] & 0xFFFF, (r[:, 6] >> 16) & 0xFFFF, r[:, 7]
+    for x, p in enumerate(PHASES):
+        out[f"c_{p}"] = r[:, 8 + x]
+    return out
 
 
 def last_launch_count() -> int:

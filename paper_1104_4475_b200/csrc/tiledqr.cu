@@ -25,6 +25,9 @@ using namespace tqr;
 // ============================================================================
 static thread_local std::string g_err;
 static thread_local int g_launches = 0;
+struct DevPlan;
+static int g_trace_on = 0;
+static DevPlan *g_trace_plan = nullptr;
 
 static int fail(int code, const std::string &msg) { g_err = msg; return code; }
 static int cuda_fail(cudaError_t e, const char *where) {
@@ -90,15 +93,15 @@ static int env_int(const char *name, int dflt) {
   return v && *v ? atoi(v) : dflt;
 }
 
+// Column-strip width of the update tasks: 32 columns = 4 n8 DMMA tiles, so the
+// W = V^T C contraction of a 32-wide block is exactly one 16x8 fragment per warp
+// (DESIGN.md §5); the last strip of a tile may be narrower.
 static int pick_ws(int nb, int ib) {
   int forced = env_int("TQR_WS", 0);
   if (forced > 0) return forced < nb ? forced : nb;
-  if (nb <= 8) return nb;
-  static const int cand[] = {64, 56, 48, 40, 32, 24, 16, 8};
-  for (int w : cand)
-    if (w <= nb && nb % w == 0 && smem_bytes(nb, ib, w) <= kMaxSmem) return w;
-  for (int w : cand)
-    if (w <= nb && smem_bytes(nb, ib, w) <= kMaxSmem) return w;
+  if (nb <= 32) return nb;
+  for (int w : {32, 24, 16, 8})
+    if (smem_bytes(nb, ib, w) <= kMaxSmem) return w;
   return 8;
 }
 
@@ -108,11 +111,13 @@ struct DevPlan {
   int32_t *deps = nullptr;
   int *done = nullptr;      // per-task completion epoch
   int *ctrl = nullptr;      // [0] = next task, [1] = CTAs exited
+  unsigned long long *trace = nullptr;   // diagnostic per-task timestamps
+  std::vector<DevTask> host_tasks;      // kept for tqr_trace_fetch
   int ntask = 0;
   int epoch = 0;
   int ws = 0;
   ~DevPlan() {
-    cudaFree(tasks); cudaFree(deps); cudaFree(done); cudaFree(ctrl);
+    cudaFree(tasks); cudaFree(deps); cudaFree(done); cudaFree(ctrl); cudaFree(trace);
   }
 };
 
@@ -122,6 +127,7 @@ static std::map<PlanKey, std::unique_ptr<DevPlan>> g_plans;
 
 static int upload(const DevGraph &g, int ws, DevPlan &pl) {
   pl.ntask = (int)g.tasks.size();
+  pl.host_tasks = g.tasks;
   pl.ws = ws;
   size_t tb = sizeof(DevTask) * (g.tasks.size() ? g.tasks.size() : 1);
   size_t db = sizeof(int32_t) * (g.deps.size() ? g.deps.size() : 1);
@@ -165,6 +171,31 @@ static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, in
 extern "C" void tqr_release_plans(void) {
   std::lock_guard<std::mutex> lk(g_mu);
   g_plans.clear();
+  g_trace_plan = nullptr;
+}
+
+extern "C" int tqr_trace_enable(int on) {
+  g_trace_on = on ? 1 : 0;
+  return 0;
+}
+
+extern "C" int64_t tqr_trace_fetch(uint64_t *out, int64_t cap) {
+  DevPlan *pl = g_trace_plan;
+  if (!pl || !pl->trace) return fail(TQR_EINVAL, "tqr_trace_fetch: no traced launch");
+  if (cap < (int64_t)pl->ntask * 16) return fail(TQR_ECAP, "tqr_trace_fetch: capacity < 16 * ntask");
+  std::vector<uint64_t> raw((size_t)pl->ntask * kTraceWords);
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(raw.data(), pl->trace, raw.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  for (int t = 0; t < pl->ntask; ++t) {
+    const DevTask &d = pl->host_tasks[t];
+    const uint64_t *r = raw.data() + (size_t)kTraceWords * t;
+    uint64_t *o = out + 16 * (size_t)t;
+    o[0] = r[0]; o[1] = r[1]; o[2] = r[2]; o[3] = r[3] >> 32;
+    o[4] = (uint64_t)d.kind; o[5] = (uint64_t)d.i | ((uint64_t)(uint16_t)d.piv << 16);
+    o[6] = (uint64_t)d.k | ((uint64_t)(uint16_t)d.j << 16); o[7] = (uint64_t)d.s;
+    for (int x = 0; x < 8; ++x) o[8 + x] = r[4 + x];
+  }
+  return pl->ntask;
 }
 
 static int check_shape(int m, int n, int nb, int ib, int &p, int &q) {
@@ -200,6 +231,12 @@ static int launch(DevPlan *pl, int p, int q, int nb, int ib, double *A, double *
   a.done = pl->done; a.ctrl = pl->ctrl; a.epoch = ++pl->epoch;
   a.A = A; a.T = T; a.C = C;
   a.p = p; a.q = q; a.nb = nb; a.ib = ib; a.ws = pl->ws; a.trans = trans;
+  a.trace = nullptr;
+  if (g_trace_on) {
+    if (!pl->trace) CUDA_TRY(cudaMalloc(&pl->trace, sizeof(unsigned long long) * kTraceWords * pl->ntask));
+    a.trace = pl->trace;
+    g_trace_plan = pl;
+  }
   int grid = sms;
   int forced = env_int("TQR_GRID", 0);
   if (forced > 0) grid = forced;

@@ -19,8 +19,9 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kMaxNb = 256;
 constexpr int kMaxIb = 32;
 constexpr size_t kMaxSmem = 227 * 1024 - 512;   // dynamic smem budget (opt-in max minus static)
-constexpr int kTld = 33;                    // ld of the 32 x 32 smem T / top / G blocks
-constexpr int kPanelScratch = 2 * 32 * kTld + kWarps * 32 + 4 * 32 + 8;
+constexpr int kTld = 33;
+constexpr int kTraceWords = 12;             // per-task trace record (diagnostics)                    // ld of the 32 x 32 smem T / top / G blocks
+constexpr int kPanelScratch = 2 * 32 * kTld + 2 * 256 + 8 + 32;
 
 struct RunArgs {
   const DevTask *tasks;
@@ -32,22 +33,29 @@ struct RunArgs {
   int nctas;
   double *A, *T, *C;
   int p, q, nb, ib, ws, trans;
+  unsigned long long *trace;   // optional: kTraceWords u64 per task (taken, ready, done, smid<<32|kind, 8 phase cycle counters)
 };
 
 struct SmemLayout {
-  int ldc, ldv;
+  int ldc, ldv, ldw, wcols;
   size_t offC, offV, offW, offT, total;   // in doubles
 };
 
-__host__ __device__ inline int odd_ld(int n) { return n | 1; }
+// Leading dimensions are = 4 (mod 16) doubles: the DMMA fragment loads of a
+// warp (lanes 4g+t reading element t + g*ld or g + t*ld) then hit 16 distinct
+// 8-byte bank pairs per half-warp (conflict-free).
+__host__ __device__ inline int ld4(int n) { return n + ((4 - n % 16) + 16) % 16; }
+__host__ __device__ inline int round_up(int n, int m) { return (n + m - 1) / m * m; }
 
 __host__ __device__ inline SmemLayout smem_layout(int nb, int ib, int ws) {
   SmemLayout s;
-  s.ldc = odd_ld(2 * nb);
-  s.ldv = odd_ld(nb);
-  size_t c = (size_t)s.ldc * ws;
-  size_t v = (size_t)s.ldv * ib;
-  size_t w = (size_t)2 * 32 * ws;
+  s.wcols = round_up(ws, 8);
+  s.ldc = ld4(2 * nb + 16);          // [C1 rows 0..nb-1 | C2 rows nb..2nb-1 | m16 padding]
+  s.ldv = ld4(round_up(nb, 16));     // V rows incl. m16 / k4 padding
+  s.ldw = 36;
+  size_t c = (size_t)s.ldc * s.wcols;
+  size_t v = (size_t)s.ldv * 32;
+  size_t w = (size_t)2 * s.ldw * s.wcols;
   if (w < (size_t)kPanelScratch) w = kPanelScratch;
   s.offC = 0;
   s.offV = c;
@@ -70,6 +78,37 @@ __device__ __forceinline__ void st_release(int *p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// ---- optional in-task phase profiling (diagnostic tracer) -------------------
+// Thread 0 attributes the cycles since the previous mark to a phase slot;
+// marks sit right after CTA-wide barriers, so they measure the whole CTA.
+__shared__ unsigned long long s_prof[8];
+__shared__ unsigned long long s_prof_last;
+__shared__ int s_prof_on;
+enum { PH_LOAD = 0, PH_FIX, PH_MMA1, PH_TRI, PH_MMA3, PH_PANEL, PH_TREC, PH_STORE };
+#ifdef TQR_PANEL_PROF
+#define PPROF(slot) prof_mark(slot)
+#else
+#define PPROF(slot)
+#endif
+__device__ __forceinline__ void prof_mark(int slot) {
+  if (threadIdx.x == 0 && s_prof_on) {
+    unsigned long long now = clock64();
+    s_prof[slot] += now - s_prof_last;
+    s_prof_last = now;
+  }
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+  return v;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned v;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(v));
+  return v;
+}
+
 __device__ __forceinline__ double *tile_ptr(double *base, int p, int nb, int i, int k) {
   return base + ((size_t)k * p + i) * (size_t)nb * nb;
 }
@@ -77,92 +116,244 @@ __device__ __forceinline__ double *tslot_ptr(double *T, int p, int nb, int ib, i
   return T + (((size_t)k * p + i) * 2 + s) * (size_t)ib * nb;
 }
 
+// ---- asynchronous global -> shared copies (LDGSTS) ---------------------------
+// All tile data reaches shared memory through cp.async so that every load of a
+// task is in flight at once (a scalar load loop is L2-latency bound). The .cg
+// (16 B) form bypasses L1; the 8 B form is used only for odd sizes. Writers of
+// a tile are ordered before readers by the release/acquire flags plus a
+// gpu-scope fence, which also invalidates L1.
+__device__ __forceinline__ void cp_async8(double *dst, const double *src) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(double *dst, const double *src) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// copy rows [r0, r1) of columns [c0, c0+ncol) of a column-major global array
+// (leading dimension ldg) to shared dst[(r - r0) + c*lds]
+__device__ __forceinline__ void async_block(double *dst, int lds, const double *src, int ldg, int r0, int r1,
+                                            int c0, int ncol) {
+  const int nr = r1 - r0;
+  if (nr <= 0 || ncol <= 0) return;
+  const double *g = src + r0 + (size_t)c0 * ldg;
+  const bool v16 = ((nr | lds | ldg) & 1) == 0 && ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  if (v16) {
+    const int h = nr >> 1;
+    for (int idx = threadIdx.x; idx < h * ncol; idx += kThreads) {
+      const int r = (idx % h) * 2, c = idx / h;
+      cp_async16(dst + r + c * lds, g + r + (size_t)c * ldg);
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < nr * ncol; idx += kThreads) {
+      const int r = idx % nr, c = idx / nr;
+      cp_async8(dst + r + c * lds, g + r + (size_t)c * ldg);
+    }
+  }
+}
+
 // ---- strip movement: rows [r0, r1) of tile columns [c0, c0+wsz) <-> buf rows (off + r)
 __device__ __forceinline__ void load_rows(double *buf, int ldc, int off, const double *tile, int nb,
                                           int r0, int r1, int c0, int wsz) {
-  const int nr = r1 - r0;
-  for (int idx = threadIdx.x; idx < nr * wsz; idx += kThreads) {
-    int r = r0 + idx % nr, c = idx / nr;
-    buf[off + r + c * ldc] = __ldcg(tile + r + (size_t)(c0 + c) * nb);
-  }
+  async_block(buf + off + r0, ldc, tile, nb, r0, r1, c0, wsz);
 }
 __device__ __forceinline__ void store_rows(const double *buf, int ldc, int off, double *tile, int nb,
                                            int r0, int r1, int c0, int wsz) {
   const int nr = r1 - r0;
-  for (int idx = threadIdx.x; idx < nr * wsz; idx += kThreads) {
-    int r = r0 + idx % nr, c = idx / nr;
-    tile[r + (size_t)(c0 + c) * nb] = buf[off + r + c * ldc];
+  if (((nr | ldc | nb | r0 | off) & 1) == 0) {
+    const int h = nr >> 1;
+    for (int idx = threadIdx.x; idx < h * wsz; idx += kThreads) {
+      const int r = r0 + (idx % h) * 2, c = idx / h;
+      *reinterpret_cast<double2 *>(tile + r + (size_t)(c0 + c) * nb) =
+          *reinterpret_cast<const double2 *>(buf + off + r + c * ldc);
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < nr * wsz; idx += kThreads) {
+      int r = r0 + idx % nr, c = idx / nr;
+      tile[r + (size_t)(c0 + c) * nb] = buf[off + r + c * ldc];
+    }
   }
 }
 
-// V of a GEQRT block (columns j0..j0+bw-1 of tile X): rows j0..nb-1, unit
-// diagonal, zeros above; stored at Vbuf[(r - j0) + l*ldv].
-__device__ __forceinline__ void load_v_geqrt(double *V, int ldv, const double *X, int nb, int j0, int bw) {
-  const int nr = nb - j0;
-  for (int idx = threadIdx.x; idx < nr * bw; idx += kThreads) {
-    int rr = idx % nr, l = idx / nr;
-    double v = 0.0;
-    if (rr == l) v = 1.0;
-    else if (rr > l) v = __ldcg(X + (j0 + rr) + (size_t)(j0 + l) * nb);
-    V[rr + l * ldv] = v;
+// V of a GEQRT block (columns j0..j0+bw-1 of tile X): rows j0..nb-1 at
+// Vbuf[(r - j0) + l*ldv]. Issued asynchronously; fix_v_geqrt (after the wait)
+// sets the unit diagonal, zeros above it and the k4 padding rows.
+__device__ __forceinline__ void issue_v_geqrt(double *V, int ldv, const double *X, int nb, int j0, int bw) {
+  async_block(V, ldv, X, nb, j0, nb, j0, bw);
+}
+__device__ __forceinline__ void fix_v_geqrt(double *V, int ldv, int nb, int j0, int bw) {
+  const int nr = nb - j0, nr4 = (nr + 3) & ~3;
+  for (int idx = threadIdx.x; idx < bw * bw; idx += kThreads) {
+    const int rr = idx % bw, l = idx / bw;
+    if (rr <= l && rr < nr) V[rr + l * ldv] = rr == l ? 1.0 : 0.0;
   }
+  const int pad = nr4 - nr;
+  for (int idx = threadIdx.x; idx < pad * bw; idx += kThreads) V[nr + idx % pad + (idx / pad) * ldv] = 0.0;
 }
 // V2 of a TTQRT (tri) / TSQRT block: rows 0..R2-1 of tile X, R2 = j0+bw (TT) or nb (TS);
 // in TT only the upper triangle (r <= j0+l) belongs to the reflectors.
-__device__ __forceinline__ void load_v_tp(double *V, int ldv, const double *X, int nb, int j0, int bw, bool tri) {
-  const int nr = tri ? j0 + bw : nb;
-  for (int idx = threadIdx.x; idx < nr * bw; idx += kThreads) {
-    int r = idx % nr, l = idx / nr;
-    V[r + l * ldv] = (!tri || r <= j0 + l) ? __ldcg(X + r + (size_t)(j0 + l) * nb) : 0.0;
-  }
+__device__ __forceinline__ void issue_v_tp(double *V, int ldv, const double *X, int nb, int j0, int bw, bool tri) {
+  async_block(V, ldv, X, nb, 0, tri ? j0 + bw : nb, j0, bw);
 }
-__device__ __forceinline__ void load_t(double *Ts, const double *Tslot, int ib, int j0, int bw) {
-  for (int idx = threadIdx.x; idx < bw * bw; idx += kThreads) {
-    int l = idx % bw, c = idx / bw;
-    Ts[l + c * kTld] = l <= c ? __ldcg(Tslot + l + (size_t)(j0 + c) * ib) : 0.0;
+__device__ __forceinline__ void fix_v_tp(double *V, int ldv, int nb, int j0, int bw, bool tri) {
+  const int nr = tri ? j0 + bw : nb, nr4 = (nr + 3) & ~3;
+  if (tri) {
+    for (int idx = threadIdx.x; idx < bw * bw; idx += kThreads) {
+      const int rr = idx % bw, l = idx / bw;
+      if (rr > l) V[j0 + rr + l * ldv] = 0.0;
+    }
+  }
+  const int pad = nr4 - nr;
+  for (int idx = threadIdx.x; idx < pad * bw; idx += kThreads) V[nr + idx % pad + (idx / pad) * ldv] = 0.0;
+}
+// zero V rows [nr, round_up(nr, 4)) of columns 0..bw-1
+__device__ __forceinline__ void zero_vpad(double *V, int ldv, int nr, int bw) {
+  const int pad = ((nr + 3) & ~3) - nr;
+  for (int idx = threadIdx.x; idx < pad * bw; idx += kThreads) V[nr + idx % pad + (idx / pad) * ldv] = 0.0;
+}
+// T block (bw x bw upper triangular) of columns j0.. of a T slot -> Ts (ld kTld);
+// the rest of the 32 x 32 block is zeroed (it feeds a padded DMMA)
+__device__ __forceinline__ void issue_t(double *Ts, const double *Tslot, int ib, int j0, int bw) {
+  for (int idx = threadIdx.x; idx < 32 * 32; idx += kThreads) {
+    const int l = idx & 31, c = idx >> 5;
+    if (l <= c && c < bw) cp_async8(Ts + l + c * kTld, Tslot + l + (size_t)(j0 + c) * ib);
+    else Ts[l + c * kTld] = 0.0;
   }
 }
 
+// ---- FP64 tensor-core MMA (DMMA): D(16x8) += A(16x4) B(4x8) ------------------
+// Fragments (lane = 4*g + t): a0 = A[g][t], a1 = A[g+8][t]; b0 = B[t][g];
+// d0,d1 = D[g][2t, 2t+1], d2,d3 = D[g+8][2t, 2t+1].
+__device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, double b0) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+               : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+               : "d"(a0), "d"(a1), "d"(b0));
+}
+
 // ---- apply one compact-WY block to a strip held in shared memory ----------
-// W = [Ctop +] V^T Cv ; W2 = op(T) W ; Cv -= V W2 ; [Ctop -= W2]
+// W = [Ctop +] V^T Cv ; W2 = -op(T) W ; Cv += V W2 ; [Ctop += W2]
 // trans: op(T) = T^T (applies Q_b^T), else T (applies Q_b).
 // Ctop (bw rows, may be null) carries the implicit identity part of
 // V = [I; V2] (TT/TS kernels). All arrays in smem, column-major.
+// Requirements (kept by the loaders): V rows [nrows, round_up(nrows,4)) are
+// zero; everything the m16/n8 padding reads is finite; W/W2 have ldw = 36.
+// Both contractions run on the FP64 tensor pipe (mma.sync m16n8k4 f64).
 __device__ void apply_block(double *Ctop, double *Cv, int ldc, int nrows, const double *V, int ldv,
                             const double *Ts, int bw, int wsz, bool trans, double *W, double *W2) {
-  for (int idx = threadIdx.x; idx < bw * wsz; idx += kThreads) {
-    int l = idx % bw, c = idx / bw;
-    double s = Ctop ? Ctop[l + c * ldc] : 0.0;
-    const double *v = V + l * ldv;
-    const double *cc = Cv + c * ldc;
-    for (int r = 0; r < nrows; ++r) s = fma(v[r], cc[r], s);
-    W[l + c * 32] = s;
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < bw * wsz; idx += kThreads) {
-    int l = idx % bw, c = idx / bw;
-    double s = 0.0;
-    if (trans) {
-      for (int m = 0; m <= l; ++m) s = fma(Ts[m + l * kTld], W[m + c * 32], s);
-    } else {
-      for (int m = l; m < bw; ++m) s = fma(Ts[l + m * kTld], W[m + c * 32], s);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  constexpr int ldw = 36;
+  // phase 1: W (bw x wsz) = V^T Cv, one 16x8 fragment per warp-iteration, full K
+  {
+    const int mt = (bw + 15) >> 4, nt = (wsz + 7) >> 3;
+    const int kpad = (nrows + 3) & ~3;
+    for (int f = warp; f < mt * nt; f += kWarps) {
+      const int m0 = (f % mt) * 16, n0 = (f / mt) * 8;
+      double acc0[4] = {0.0, 0.0, 0.0, 0.0}, acc1[4] = {0.0, 0.0, 0.0, 0.0};
+      const double *va = V + (m0 + g) * ldv + t;
+      const double *vb = va + 8 * ldv;
+      const double *cb = Cv + (n0 + g) * ldc + t;
+      int k = 0;
+      for (; k + 8 <= kpad; k += 8) {
+        dmma(acc0, va[k], vb[k], cb[k]);
+        dmma(acc1, va[k + 4], vb[k + 4], cb[k + 4]);
+      }
+      if (k < kpad) dmma(acc0, va[k], vb[k], cb[k]);
+      const int r0 = m0 + g, c0 = n0 + 2 * t;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = r0 + (e >> 1) * 8, c = c0 + (e & 1);
+        double v = acc0[e] + acc1[e];
+        if (Ctop && r < bw && c < wsz) v += Ctop[r + c * ldc];
+        W[r + c * ldw] = v;
+      }
     }
-    W2[l + c * 32] = s;
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < nrows * wsz; idx += kThreads) {
-    int r = idx % nrows, c = idx / nrows;
-    double s = 0.0;
-    for (int l = 0; l < bw; ++l) s = fma(V[r + l * ldv], W2[l + c * 32], s);
-    Cv[r + c * ldc] -= s;
+  prof_mark(PH_MMA1);
+  // phase 2: W2 = -op(T) W on the tensor pipe (T is a zero-padded 32 x 32
+  // upper triangle, so rows bw..31 of W2 come out exactly zero)
+  const int kpad3 = (bw + 3) & ~3;
+  {
+    const int nt = (wsz + 7) >> 3;
+    for (int f = warp; f < 2 * nt; f += kWarps) {
+      const int m0 = (f & 1) * 16, n0 = (f >> 1) * 8;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k = 0; k < kpad3; k += 4) {
+        double a0, a1;
+        if (trans) {   // A[l][m] = T[m][l]
+          a0 = Ts[(k + t) + (m0 + g) * kTld];
+          a1 = Ts[(k + t) + (m0 + g + 8) * kTld];
+        } else {       // A[l][m] = T[l][m]
+          a0 = Ts[(m0 + g) + (k + t) * kTld];
+          a1 = Ts[(m0 + g + 8) + (k + t) * kTld];
+        }
+        dmma(acc, a0, a1, W[(k + t) + (n0 + g) * ldw]);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = m0 + g + (e >> 1) * 8, c = n0 + 2 * t + (e & 1);
+        W2[r + c * ldw] = -acc[e];
+      }
+    }
+  }
+  __syncthreads();
+  prof_mark(PH_TRI);
+  // phase 3: Cv (nrows x wsz) += V W2; warp w owns m-tiles w, w+8 and all n-tiles
+  {
+    const int mt = (nrows + 15) >> 4, nt = (wsz + 7) >> 3;
+    double acc[2][8][4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int m0 = (warp + j * kWarps) * 16;
+#pragma unroll
+      for (int n = 0; n < 8; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = m0 + g + (e >> 1) * 8, c = n * 8 + 2 * t + (e & 1);
+          acc[j][n][e] = (m0 < nrows && n < nt) ? Cv[r + c * ldc] : 0.0;
+        }
+    }
+    for (int k = 0; k < kpad3; k += 4) {
+      double b[8];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) b[n] = n < nt ? W2[(k + t) + (n * 8 + g) * ldw] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int m0 = (warp + j * kWarps) * 16;
+        if (warp + j * kWarps < mt) {
+          const double a0 = V[(m0 + g) + (k + t) * ldv];
+          const double a1 = V[(m0 + g + 8) + (k + t) * ldv];
+#pragma unroll
+          for (int n = 0; n < 8; ++n)
+            if (n < nt) dmma(acc[j][n], a0, a1, b[n]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int m0 = (warp + j * kWarps) * 16;
+      if (m0 < nrows) {
+#pragma unroll
+        for (int n = 0; n < 8; ++n)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = m0 + g + (e >> 1) * 8, c = n * 8 + 2 * t + (e & 1);
+            if (n < nt && r < nrows && c < wsz) Cv[r + c * ldc] = acc[j][n][e];
+          }
+      }
+    }
   }
   if (Ctop) {
     for (int idx = threadIdx.x; idx < bw * wsz; idx += kThreads) {
-      int l = idx % bw, c = idx / bw;
-      Ctop[l + c * ldc] -= W2[l + c * 32];
+      const int l = idx % bw, c = idx / bw;
+      Ctop[l + c * ldc] += W2[l + c * ldw];
     }
   }
   __syncthreads();
+  prof_mark(PH_MMA3);
 }
 
 // ---- warp reduce-scatter: lane l ends with sum over lanes of v[l] (v[0]) ----
@@ -177,145 +368,247 @@ __device__ __forceinline__ void rs_step(double (&v)[32], int lane) {
   }
 }
 
+// ---- Householder scalars (xLARFG) from alpha and ||x||^2 ------------------
+// beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha)/beta, scale =
+// 1/(alpha - beta), evaluated with one rsqrt and one reciprocal:
+// r = 1/||(alpha,x)||, tau = 1 + |alpha| r, scale = sign(alpha)/(|alpha| + ||.||).
+// (Equal to the textbook formulas up to rounding; reading R8.)
+__device__ __forceinline__ void larfg_scalars(double alpha, double xn2, double &beta, double &tau, double &scale) {
+  if (xn2 == 0.0) {
+    beta = alpha; tau = 0.0; scale = 0.0;
+    return;
+  }
+  const double s = fma(alpha, alpha, xn2);
+  const double aa = fabs(alpha);
+  double nrm, r;
+  if (s < 1e-290 || s > 1e290) {          // extreme range: scaled hypot
+    nrm = hypot(alpha, sqrt(xn2));
+    r = 1.0 / nrm;
+  } else {
+    r = rsqrt(s);
+    nrm = s * r;
+  }
+  beta = alpha >= 0.0 ? -nrm : nrm;
+  tau = fma(aa, r, 1.0);
+  const double rs = 1.0 / (aa + nrm);
+  scale = alpha >= 0.0 ? rs : -rs;
+}
+
+// ---- T from G = V^T V and tau by recursive doubling -------------------------
+// Block form of the compact-WY product (lines 62-66): for Q1 Q2 with
+// Q_i = I - V_i T_i V_i^T,  T = [[T1, -T1 (V1^T V2) T2], [0, T2]].
+// Levels s = 1, 2, 4, 8, 16 merge adjacent diagonal blocks; every level is two
+// small triangular products spread over the CTA (one entry per thread).
+// Ts must hold tau on the diagonal and zeros elsewhere on entry; X is scratch.
+__device__ void t_doubling(double *Ts, const double *G, double *X) {
+  const int tid = threadIdx.x;
+  for (int sz = 1; sz < 32; sz <<= 1) {
+    const int per = sz * sz, n = (16 / sz) * per;      // entries per merge, total (= 16*sz <= 256)
+    if (tid < n) {                                       // X = G12 T22
+      const int u = tid / per, e = tid % per, i = e % sz, j = e / sz;
+      const int b0 = 2 * sz * u, b1 = b0 + sz;
+      double acc = 0.0;
+      for (int m = 0; m <= j; ++m) acc = fma(G[(b0 + i) + (b1 + m) * kTld], Ts[(b1 + m) + (b1 + j) * kTld], acc);
+      X[(b0 + i) + (b1 + j) * kTld] = acc;
+    }
+    __syncthreads();
+    if (tid < n) {                                       // T12 = -T11 X
+      const int u = tid / per, e = tid % per, i = e % sz, j = e / sz;
+      const int b0 = 2 * sz * u, b1 = b0 + sz;
+      double acc = 0.0;
+      for (int m = i; m < sz; ++m) acc = fma(Ts[(b0 + i) + (b0 + m) * kTld], X[(b0 + m) + (b1 + j) * kTld], acc);
+      Ts[(b0 + i) + (b1 + j) * kTld] = -acc;
+    }
+    __syncthreads();
+  }
+}
+
+// G (32 x 32, ld kTld) = V^T V for the 32 V columns in Vbuf (rows 0..nr4-1), DMMA
+__device__ void gram_v(double *G, const double *V, int ldv, int nr) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int m0 = (warp & 1) * 16, n0 = (warp >> 1) * 8;   // 8 warps = 2 x 4 fragments
+  const int kpad = (nr + 3) & ~3;
+  double acc0[4] = {0.0, 0.0, 0.0, 0.0}, acc1[4] = {0.0, 0.0, 0.0, 0.0};
+  const double *va = V + (m0 + g) * ldv + t, *vb = va + 8 * ldv, *vc = V + (n0 + g) * ldv + t;
+  int k = 0;
+  for (; k + 8 <= kpad; k += 8) {
+    dmma(acc0, va[k], vb[k], vc[k]);
+    dmma(acc1, va[k + 4], vb[k + 4], vc[k + 4]);
+  }
+  if (k < kpad) dmma(acc0, va[k], vb[k], vc[k]);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) G[(m0 + g + (e >> 1) * 8) + (n0 + 2 * t + (e & 1)) * kTld] = acc0[e] + acc1[e];
+}
+
 // ---- panel factorization of one inner block --------------------------------
 // MODE 0 = GEQRT on tile X (rows j0..nb-1, pivot row j0+c for column c)
 // MODE 1 = TTQRT: pivot rows = A1 rows j0..j0+bw-1 (triangle), eliminated
 //          rows = A2 rows 0..j0+c (triangle)           (Table 1)
 // MODE 2 = TSQRT: eliminated rows = all nb rows of A2 (line 246)
-// Each thread owns one eliminated row in registers; one fused block
-// reduction per column produces ||x||^2, the dot products of the update and
-// the V^T v column of the T recurrence. Writes R/V back (only the parts this
-// kernel owns), fills Vbuf (for the trailing update) and Ts, stores T.
+// Column-cyclic warp ownership: warp w owns panel columns w, w+8, w+16, w+24;
+// lane l holds rows l, l+32, ..., l+224 of them in registers (TT/TS: lane l
+// also holds pivot row l of each owned column). Reflector c is generated by
+// its owner warp alone (warp-local norm, xLARFG scalars), published through
+// shared memory, and after ONE barrier every warp applies it to its own
+// columns > c (warp-local dot products). The owner of column c+1 can start
+// as soon as its column is updated, so the per-column chain is short.
+// After the columns: G = V^T V on the tensor pipe and T by recursive
+// doubling. Writes R/V back (only the parts this kernel owns), fills Vbuf (for
+// a trailing update), Ts and the T slot.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 template <int MODE>
 __device__ void panel_block(double *X, double *A1, double *Tslot, int nb, int ib, int j0, int bw,
                             double *Vbuf, int ldv, double *Ts, double *scratch) {
-  double *top = scratch;               // 32 x 33 (TT/TS pivot rows)
-  double *G = top + 32 * kTld;         // 32 x 33, G[m + c*33] = V_m^T v_c
-  double *red = G + 32 * kTld;         // kWarps x 32
-  double *prow = red + kWarps * 32;    // pivot row (GEQRT)
-  double *wv = prow + 32;
-  double *taus = wv + 32;
-  double *sc = taus + 32;
+  double *top = scratch;               // 32 x kTld scratch for t_doubling
+  double *G = top + 32 * kTld;         // 32 x kTld: V^T V
+  double *vsh = G + 32 * kTld;         // 2 x 256: published reflector (double-buffered)
+  double *scal = vsh + 2 * 256;        // 2 x 4: tau of the published reflector
+  double *taus = scal + 8;             // 32
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int row = MODE == 0 ? j0 + tid : tid;
-  const bool valid = MODE == 0 ? row < nb : (MODE == 1 ? row < j0 + bw : row < nb);
+  const int nr = MODE == 0 ? nb - j0 : (MODE == 1 ? j0 + bw : nb);   // V rows of this block
+  const int rbase = MODE == 0 ? j0 : 0;
 
-  double a[32];
+  double a[4][8];     // a[q][s]: column warp + 8q, row rbase + lane + 32 s
+  double pt[4];       // TT/TS: A1 row j0+lane of column warp + 8q (pivot rows)
 #pragma unroll
-  for (int c = 0; c < 32; ++c) {
-    a[c] = 0.0;
-    if (valid && c < bw && (MODE != 1 || row <= j0 + c)) a[c] = __ldcg(X + row + (size_t)(j0 + c) * nb);
-  }
-  if (MODE != 0) {
-    for (int idx = tid; idx < 32 * 32; idx += kThreads) {
-      int l = idx & 31, c = idx >> 5;
-      top[l + c * kTld] = (l < bw && c < bw && l <= c) ? __ldcg(A1 + (j0 + l) + (size_t)(j0 + c) * nb) : 0.0;
+  for (int q = 0; q < 4; ++q) {
+    const int cl = warp + 8 * q;
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2) {
+      const int rr = lane + 32 * s2, row = rbase + rr;
+      a[q][s2] = (cl < bw && rr < nr && (MODE != 1 || row <= j0 + cl)) ? __ldcg(X + row + (size_t)(j0 + cl) * nb) : 0.0;
     }
+    pt[q] = (MODE != 0 && cl < bw && lane <= cl) ? __ldcg(A1 + (j0 + lane) + (size_t)(j0 + cl) * nb) : 0.0;
   }
-  __syncthreads();
 
+  double betas[4] = {0.0, 0.0, 0.0, 0.0};   // R diagonal of owned columns (lane c of owner)
+#pragma unroll 1
+  for (int c = 0; c < bw; ++c) {
+    const int qo = c >> 3, wo = c & 7;
+    const int pr = j0 + c;
+    double *vb = vsh + (c & 1) * 256;
+    PPROF(PH_STORE);
+    if (warp == wo) {
+      // ---- generate reflector c from the owned column a[qo][*] ----
+      double col[8];
 #pragma unroll
-  for (int c = 0; c < 32; ++c) {
-    if (c < bw) {
-      const int pr = j0 + c;
-      if (MODE == 0 && row == pr) {
+      for (int s2 = 0; s2 < 8; ++s2)
+        col[s2] = qo == 0 ? a[0][s2] : (qo == 1 ? a[1][s2] : (qo == 2 ? a[2][s2] : a[3][s2]));
+      const double ptq = qo == 0 ? pt[0] : (qo == 1 ? pt[1] : (qo == 2 ? pt[2] : pt[3]));
+      const int first = MODE == 0 ? c + 1 : 0;                 // first participating relative row
+      const int last = MODE == 1 ? pr : nr - 1;                // last participating relative row
+      double ss = 0.0;
 #pragma unroll
-        for (int l = 0; l < 32; ++l) prow[l] = a[l];
+      for (int s2 = 0; s2 < 8; ++s2) {
+        const int rr = lane + 32 * s2;
+        if (rr >= first && rr <= last) ss = fma(col[s2], col[s2], ss);
       }
-      const bool part = valid && (MODE == 0 ? row > pr : (MODE == 1 ? row <= pr : true));
-      const double x = part ? a[c] : 0.0;
-      double v[32];
+      const double xn2 = warp_sum(ss);
+      PPROF(PH_LOAD);
+      const double alpha = __shfl_sync(0xffffffffu, MODE == 0 ? col[0] : ptq, c);
+      double beta, tau, scale;
+      larfg_scalars(alpha, xn2, beta, tau, scale);
+      PPROF(PH_FIX);
 #pragma unroll
-      for (int l = 0; l < 32; ++l) v[l] = x * a[l];
-      rs_step<16>(v, lane);
-      rs_step<8>(v, lane);
-      rs_step<4>(v, lane);
-      rs_step<2>(v, lane);
-      rs_step<1>(v, lane);
-      red[warp * 32 + lane] = v[0];
-      __syncthreads();
-      if (warp == 0) {
-        double tot = 0.0;
+      for (int s2 = 0; s2 < 8; ++s2) {
+        const int rr = lane + 32 * s2;
+        const double v = (rr >= first && rr <= last) ? scale * col[s2] : 0.0;
+        vb[rr] = v;
+        if (rr >= first && rr <= last) col[s2] = v;               // column now holds V below the pivot
+      }
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) tot += red[w * 32 + lane];
-        const double Pl = MODE == 0 ? prow[lane] : top[c + lane * kTld];
-        const double alpha = __shfl_sync(0xffffffffu, Pl, c);
-        const double xn2 = __shfl_sync(0xffffffffu, tot, c);
-        double tau, scale, beta;
-        if (xn2 == 0.0) {
-          tau = 0.0; scale = 0.0; beta = alpha;
-        } else {
-          const double xn = sqrt(xn2);
-          beta = -copysign(hypot(alpha, xn), alpha);
-          tau = (beta - alpha) / beta;
-          scale = 1.0 / (alpha - beta);
+      for (int q = 0; q < 4; ++q)
+        if (q == qo) {
+#pragma unroll
+          for (int s2 = 0; s2 < 8; ++s2) a[q][s2] = col[s2];
+          if (lane == c) betas[q] = beta;
         }
-        if (lane > c && lane < bw) {
-          const double w = Pl + scale * tot;
-          wv[lane] = w;
-          if (MODE != 0) top[c + lane * kTld] = Pl - tau * w;
-        }
-        if (lane < c) G[lane + c * kTld] = (MODE == 0 ? Pl : 0.0) + scale * tot;
+      if (lane == 0) { scal[(c & 1) * 4] = tau; taus[c] = tau; }
+      PPROF(PH_MMA1);
+    }
+    __syncthreads();
+    PPROF(PH_TRI);
+    // ---- apply reflector c to the owned columns > c ----
+    // branch-free over the 4 owned columns so the 4 warp reductions overlap
+    const double tau = scal[(c & 1) * 4];
+    if (warp + 8 * 3 > c && tau != 0.0) {
+      double v[8];
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) v[s2] = vb[lane + 32 * s2];
+      double d[4], P[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        d[q] = 0.0;
+#pragma unroll
+        for (int s2 = 0; s2 < 8; ++s2) d[q] = fma(v[s2], a[q][s2], d[q]);
+        P[q] = MODE == 0 ? __shfl_sync(0xffffffffu, a[q][0], c) : __shfl_sync(0xffffffffu, pt[q], c);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) d[q] += __shfl_xor_sync(0xffffffffu, d[q], o);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int cl = warp + 8 * q;
+        const double tw = (cl > c && cl < bw) ? tau * (P[q] + d[q]) : 0.0;
+#pragma unroll
+        for (int s2 = 0; s2 < 8; ++s2) a[q][s2] = fma(-tw, v[s2], a[q][s2]);
         if (lane == c) {
-          taus[c] = tau;
-          sc[0] = scale; sc[1] = tau; sc[2] = beta;
-          if (MODE != 0) top[c + c * kTld] = beta;
+          if (MODE == 0) a[q][0] -= tw;
+          else pt[q] -= tw;
         }
       }
-      __syncthreads();
-      const double scale = sc[0], tau = sc[1];
-      if (part) {
-        const double vr = scale * x;
-        const double tv = tau * vr;
-        a[c] = vr;
-#pragma unroll
-        for (int l = c + 1; l < 32; ++l)
-          if (l < bw) a[l] -= tv * wv[l];
-      } else if (MODE == 0 && row == pr) {
-        a[c] = sc[2];
-#pragma unroll
-        for (int l = c + 1; l < 32; ++l)
-          if (l < bw) a[l] -= tau * wv[l];
-      }
     }
+    PPROF(PH_MMA3);
   }
-
-  // write back what this kernel owns + the V buffer of the trailing update
-  if (valid) {
+  // ---- write back the owned columns: X (R above / V below the pivot) and Vbuf ----
 #pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      if (c < bw) {
-        if (MODE == 0) {
-          X[row + (size_t)(j0 + c) * nb] = a[c];
-          const int rr = row - j0;
-          Vbuf[rr + c * ldv] = rr == c ? 1.0 : (rr > c ? a[c] : 0.0);
-        } else {
-          if (MODE == 2 || row <= j0 + c) X[row + (size_t)(j0 + c) * nb] = a[c];
-          Vbuf[row + c * ldv] = a[c];
+  for (int q = 0; q < 4; ++q) {
+    const int cl = warp + 8 * q;
+    if (cl < bw) {
+      if (MODE != 0 && lane == cl) pt[q] = betas[q];
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) {
+        const int rr = lane + 32 * s2, row = rbase + rr;
+        if (rr < nr) {
+          if (MODE == 0) {
+            const double fin = rr == cl ? betas[q] : a[q][s2];
+            X[row + (size_t)(j0 + cl) * nb] = fin;
+            Vbuf[rr + cl * ldv] = rr == cl ? 1.0 : (rr > cl ? a[q][s2] : 0.0);
+          } else {
+            const bool part = MODE == 2 || row <= j0 + cl;
+            if (part) X[row + (size_t)(j0 + cl) * nb] = a[q][s2];
+            Vbuf[rr + cl * ldv] = part ? a[q][s2] : 0.0;
+          }
         }
       }
     }
   }
-  if (MODE != 0) {
-    for (int idx = tid; idx < bw * bw; idx += kThreads) {
-      int l = idx % bw, c = idx / bw;
-      if (l <= c) A1[(j0 + l) + (size_t)(j0 + c) * nb] = top[l + c * kTld];
-    }
-  }
-  // T recurrence: T[c][c] = tau_c, T[0:c, c] = -tau_c T[0:c, 0:c] G[0:c, c]
-  if (warp == 0) {
-    for (int c = 0; c < bw; ++c) {
-      double t = 0.0;
-      if (lane < c)
-        for (int m = lane; m < c; ++m) t = fma(Ts[lane + m * kTld], G[m + c * kTld], t);
-      __syncwarp();
-      if (lane < c) Ts[lane + c * kTld] = -taus[c] * t;
-      else if (lane == c) Ts[c + c * kTld] = taus[c];
-      else Ts[lane + c * kTld] = 0.0;
-      __syncwarp();
+  if (MODE != 0) {     // final pivot rows (R) back to A1, upper triangle of the block
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int cl = warp + 8 * q;
+      if (cl < bw && lane <= cl) A1[(j0 + lane) + (size_t)(j0 + cl) * nb] = pt[q];
     }
   }
   __syncthreads();
+  zero_vpad(Vbuf, ldv, nr, bw);
+  for (int idx = tid; idx < 32 * 32; idx += kThreads) {     // Ts = diag(tau) (zero-padded)
+    const int l = idx & 31, c = idx >> 5;
+    Ts[l + c * kTld] = (l == c && c < bw) ? taus[c] : 0.0;
+  }
+  __syncthreads();
+  prof_mark(PH_PANEL);
+  gram_v(G, Vbuf, ldv, nr);
+  __syncthreads();
+  t_doubling(Ts, G, top);
+  prof_mark(PH_TREC);
   for (int idx = tid; idx < ib * bw; idx += kThreads) {
     int l = idx % ib, c = idx / ib;
     Tslot[l + (size_t)(j0 + c) * ib] = (l < bw && l <= c) ? Ts[l + c * kTld] : 0.0;
@@ -336,15 +629,19 @@ __device__ void panel_task(double *X, double *A1, double *Tslot, int nb, int ib,
       __syncthreads();
       if (MODE == 0) {
         load_rows(Cb, L.ldc, 0, X, nb, j0, nb, cs, wsz);
+        cp_async_wait_all();
         __syncthreads();
-        apply_block(nullptr, Cb + j0, L.ldc, nb - j0, Vb, L.ldv, Ts, bw, wsz, true, Wb, Wb + 32 * ws);
+        prof_mark(PH_LOAD);
+        apply_block(nullptr, Cb + j0, L.ldc, nb - j0, Vb, L.ldv, Ts, bw, wsz, true, Wb, Wb + L.ldw * L.wcols);
         store_rows(Cb, L.ldc, 0, X, nb, j0, nb, cs, wsz);
       } else {
         const int r2 = MODE == 1 ? j0 + bw : nb;
         load_rows(Cb, L.ldc, 0, A1, nb, j0, j0 + bw, cs, wsz);
         load_rows(Cb, L.ldc, nb, X, nb, 0, r2, cs, wsz);
+        cp_async_wait_all();
         __syncthreads();
-        apply_block(Cb + j0, Cb + nb, L.ldc, r2, Vb, L.ldv, Ts, bw, wsz, true, Wb, Wb + 32 * ws);
+        prof_mark(PH_LOAD);
+        apply_block(Cb + j0, Cb + nb, L.ldc, r2, Vb, L.ldv, Ts, bw, wsz, true, Wb, Wb + L.ldw * L.wcols);
         store_rows(Cb, L.ldc, 0, A1, nb, j0, j0 + bw, cs, wsz);
         store_rows(Cb, L.ldc, nb, X, nb, 0, r2, cs, wsz);
       }
@@ -356,24 +653,29 @@ __device__ void panel_task(double *X, double *A1, double *Tslot, int nb, int ib,
 // ---- update kernels on one column strip -----------------------------------
 // UNMQR: C (tile strip) <- Q^T C with the GEQRT reflectors of tile Vt
 __device__ void unmqr_strip(const double *Vt, const double *Tslot, double *Ct, int nb, int ib, int cs,
-                            int wsz, bool trans, int ws, double *smem, const SmemLayout &L) {
+                            int wsz, bool trans, double *smem, const SmemLayout &L) {
   double *Cb = smem + L.offC, *Vb = smem + L.offV, *Wb = smem + L.offW, *Ts = smem + L.offT;
   load_rows(Cb, L.ldc, 0, Ct, nb, 0, nb, cs, wsz);
   const int nblk = (nb + ib - 1) / ib;
   for (int t = 0; t < nblk; ++t) {
     const int b = trans ? t : nblk - 1 - t;
     const int j0 = b * ib, bw = min(ib, nb - j0);
-    load_v_geqrt(Vb, L.ldv, Vt, nb, j0, bw);
-    load_t(Ts, Tslot, ib, j0, bw);
+    issue_v_geqrt(Vb, L.ldv, Vt, nb, j0, bw);
+    issue_t(Ts, Tslot, ib, j0, bw);
+    cp_async_wait_all();
     __syncthreads();
-    apply_block(nullptr, Cb + j0, L.ldc, nb - j0, Vb, L.ldv, Ts, bw, wsz, trans, Wb, Wb + 32 * ws);
+    prof_mark(PH_LOAD);
+    fix_v_geqrt(Vb, L.ldv, nb, j0, bw);
+    __syncthreads();
+    prof_mark(PH_FIX);
+    apply_block(nullptr, Cb + j0, L.ldc, nb - j0, Vb, L.ldv, Ts, bw, wsz, trans, Wb, Wb + L.ldw * L.wcols);
   }
   store_rows(Cb, L.ldc, 0, Ct, nb, 0, nb, cs, wsz);
 }
 
 // TTMQR / TSMQR: [C1; C2] <- Q^T [C1; C2] with the TTQRT/TSQRT reflectors V2 of tile Vt
 __device__ void tpmqr_strip(const double *Vt, const double *Tslot, double *C1, double *C2, int nb, int ib,
-                            int cs, int wsz, bool tri, bool trans, int ws, double *smem, const SmemLayout &L) {
+                            int cs, int wsz, bool tri, bool trans, double *smem, const SmemLayout &L) {
   double *Cb = smem + L.offC, *Vb = smem + L.offV, *Wb = smem + L.offW, *Ts = smem + L.offT;
   load_rows(Cb, L.ldc, 0, C1, nb, 0, nb, cs, wsz);
   load_rows(Cb, L.ldc, nb, C2, nb, 0, nb, cs, wsz);
@@ -381,10 +683,15 @@ __device__ void tpmqr_strip(const double *Vt, const double *Tslot, double *C1, d
   for (int t = 0; t < nblk; ++t) {
     const int b = trans ? t : nblk - 1 - t;
     const int j0 = b * ib, bw = min(ib, nb - j0);
-    load_v_tp(Vb, L.ldv, Vt, nb, j0, bw, tri);
-    load_t(Ts, Tslot, ib, j0, bw);
+    issue_v_tp(Vb, L.ldv, Vt, nb, j0, bw, tri);
+    issue_t(Ts, Tslot, ib, j0, bw);
+    cp_async_wait_all();
     __syncthreads();
-    apply_block(Cb + j0, Cb + nb, L.ldc, tri ? j0 + bw : nb, Vb, L.ldv, Ts, bw, wsz, trans, Wb, Wb + 32 * ws);
+    prof_mark(PH_LOAD);
+    fix_v_tp(Vb, L.ldv, nb, j0, bw, tri);
+    __syncthreads();
+    prof_mark(PH_FIX);
+    apply_block(Cb + j0, Cb + nb, L.ldc, tri ? j0 + bw : nb, Vb, L.ldv, Ts, bw, wsz, trans, Wb, Wb + L.ldw * L.wcols);
   }
   store_rows(Cb, L.ldc, 0, C1, nb, 0, nb, cs, wsz);
   store_rows(Cb, L.ldc, nb, C2, nb, 0, nb, cs, wsz);
@@ -410,7 +717,7 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
       double *Cbase = t.kind == K_UNMQR ? a.A : a.C;
       const int cs = t.s * ws, wsz = min(ws, nb - cs);
       unmqr_strip(tile_ptr(a.A, p, nb, t.i, t.k), tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0),
-                  tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs, wsz, a.trans != 0, ws, smem, L);
+                  tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs, wsz, a.trans != 0, smem, L);
       break;
     }
     case K_TTMQR:
@@ -423,7 +730,7 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
       const int cs = t.s * ws, wsz = min(ws, nb - cs);
       tpmqr_strip(tile_ptr(a.A, p, nb, t.i, t.k), tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1),
                   tile_ptr(Cbase, p, nb, t.piv, t.j), tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs, wsz, tri,
-                  a.trans != 0, ws, smem, L);
+                  a.trans != 0, smem, L);
       break;
     }
     default:
@@ -440,23 +747,41 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_task;
   const SmemLayout L = smem_layout(a.nb, a.ib, a.ws);
+  if (threadIdx.x == 0) s_prof_on = 0;
+  // everything the DMMA padding may read must be finite: start from zeros
+  for (size_t x = threadIdx.x; x < L.total; x += kThreads) smem[x] = 0.0;
   for (;;) {
     if (threadIdx.x == 0) s_task = atomicAdd(&a.ctrl[0], 1);
     __syncthreads();
     const int t = s_task;
     if (t >= a.ntask) break;
     const DevTask tk = a.tasks[t];
+    unsigned long long t_take = 0, t_ready = 0;
+    if (a.trace && threadIdx.x == 0) t_take = globaltimer();
     for (int d = tk.dep_begin + threadIdx.x; d < tk.dep_end; d += kThreads) {
       const int *f = a.done + a.deps[d];
       while (ld_acquire(f) != a.epoch) __nanosleep(32);
     }
     __threadfence();
     __syncthreads();
+    if (a.trace && threadIdx.x == 0) {
+      t_ready = globaltimer();
+      for (int x = 0; x < 8; ++x) s_prof[x] = 0;
+      s_prof_last = clock64();
+      s_prof_on = 1;
+    }
     run_task(a, tk, smem, L);
     __syncthreads();
+    prof_mark(PH_STORE);
     if (threadIdx.x == 0) {
       __threadfence();
       st_release(a.done + t, a.epoch);
+      if (a.trace) {
+        unsigned long long *tr = a.trace + kTraceWords * (size_t)t;
+        tr[0] = t_take; tr[1] = t_ready; tr[2] = globaltimer();
+        tr[3] = ((unsigned long long)smid() << 32) | (unsigned)tk.kind;
+        for (int x = 0; x < 8; ++x) tr[4 + x] = s_prof[x];
+      }
     }
   }
   if (threadIdx.x == 0) {

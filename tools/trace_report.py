@@ -1,0 +1,62 @@
+"""Per-task trace of one tiled_qr launch: durations per kernel kind, waiting,
+SM utilisation (development aid; uses the library's diagnostic tracer).
+
+    python tools/trace_report.py [p q nb ib tree[:bs] [out.npy]]
+"""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+import paper_1104_4475_b200 as tq  # noqa: E402
+
+a = sys.argv[1:]
+p, q, nb, ib = (int(x) for x in (a[:4] if len(a) >= 4 else (40, 10, 200, 32)))
+tree, bs = ((a[4] if len(a) > 4 else "greedy").split(":") + ["1"])[:2]
+bs = int(bs)
+m, n = p * nb, q * nb
+g = torch.Generator(device="cuda").manual_seed(0)
+A0 = torch.randn(m * n, dtype=torch.float64, device="cuda", generator=g)
+A = torch.empty_like(A0)
+T = torch.zeros(tq.t_size(m, n, nb, ib), dtype=torch.float64, device="cuda")
+for it in range(3):
+    A.copy_(A0)
+    if it == 2:
+        tq.trace_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    tq.tiled_qr(A, m, n, nb, ib, tree, bs, "TT", T=T)
+    e1.record()
+    torch.cuda.synchronize()
+tq.trace_enable(False)
+ms = e0.elapsed_time(e1)
+tr = tq.trace_fetch()
+if len(a) > 5:
+    np.save(a[5], tr)
+t0 = tr["taken"].min()
+span = (tr["done"].max() - t0) / 1e3
+run = (tr["done"] - tr["ready"]) / 1e3
+wait = (tr["ready"] - tr["taken"]) / 1e3
+nsm = len(np.unique(tr["sm"]))
+print(f"{tree}:{bs} p={p} q={q} nb={nb} ib={ib}: event {ms:.3f} ms, traced span {span / 1e3:.3f} ms, "
+      f"{len(tr)} tasks on {nsm} SMs")
+print(f"  busy (sum run) / (SMs x span) = {run.sum() / (nsm * span):.3f};  waiting share = {wait.sum() / (nsm * span):.3f}")
+unit = nb ** 3 / 3.0
+W = {0: 4, 1: 6, 2: 2, 3: 6, 4: 6, 5: 12}
+S = -(-nb // 32) if nb > 32 else 1
+for kd in np.unique(tr["kind"]):
+    sel = tr["kind"] == kd
+    r = run[sel]
+    fl = W.get(int(kd), 0) * unit / (S if kd in (1, 3, 5) else 1)
+    print(f"  {tq.KIND_NAMES[kd]:8s} n={sel.sum():6d} run mean {r.mean():8.2f} us  p50 {np.median(r):8.2f}  "
+          f"max {r.max():8.2f}  sum {r.sum() / 1e3:8.2f} ms  ~{fl / (r.mean() * 1e3):6.1f} GFLOP/s/SM   "
+          f"wait mean {wait[sel].mean():7.2f} us")
+    cyc = {p: tr[f"c_{p}"][sel].mean() for p in tq.PHASES}
+    tot = sum(cyc.values())
+    print("           phases (kcycles/task): " + "  ".join(f"{p}={cyc[p] / 1e3:.1f}" for p in tq.PHASES if cyc[p] > 0)
+          + f"  total={tot / 1e3:.1f}")
+# critical chain: walk back from the last-finishing task through the latest-finishing... (approx: by time)
+order = np.argsort(tr["ready"])
+first = (tr["ready"] - t0) / 1e3
+print(f"  tasks started in first 10% of span: {(first < 0.1 * span).sum()}, last 10%: {(first > 0.9 * span).sum()}")
