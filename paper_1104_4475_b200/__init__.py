@@ -183,7 +183,8 @@ def trace_enable(on: bool = True):
     lib().tqr_trace_enable(1 if on else 0)
 
 
-KIND_NAMES = ["GEQRT", "UNMQR", "TTQRT", "TTMQR", "TSQRT", "TSMQR", "AP_UNMQR", "AP_TTMQR", "AP_TSMQR"]
+KIND_NAMES = ["GEQRT", "UNMQR", "TTQRT", "TTMQR", "TSQRT", "TSMQR", "AP_UNMQR", "AP_TTMQR", "AP_TSMQR",
+              "GEQRT_B", "GEQRT_U", "TTQRT_B", "TTQRT_U", "TSQRT_B", "TSQRT_U"]
 
 
 PHASES = ["load", "fix", "mma1", "tri", "mma3", "panel", "trec", "store"]

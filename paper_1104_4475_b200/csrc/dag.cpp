@@ -107,14 +107,14 @@ void reorder(DevGraph &g, const std::vector<std::pair<int64_t, int64_t>> &key,
 DevTask mk(int kind, int i, int piv, int k, int j, int s) {
   DevTask t;
   t.kind = (int16_t)kind; t.i = (int16_t)i; t.piv = (int16_t)piv; t.k = (int16_t)k;
-  t.j = (int16_t)j; t.s = (int16_t)s; t.dep_begin = t.dep_end = 0; t.pad = 0;
+  t.j = (int16_t)j; t.s = (int16_t)s; t.dep_begin = t.dep_end = 0; t.meta = 0;
   return t;
 }
 
 }  // namespace
 
 void build_factor_graph(const std::vector<TileTask> &tt, const std::vector<int64_t> &start,
-                        int p, int q, int nb, int ws, DevGraph &g) {
+                        int p, int q, int nb, int ws, bool split_panels, DevGraph &g) {
   const int S = (nb + ws - 1) / ws;
   g.tasks.clear();
   std::vector<std::vector<int>> deps;
@@ -122,7 +122,8 @@ void build_factor_graph(const std::vector<TileTask> &tt, const std::vector<int64
   // last device writer of every (tile, strip); tiles 0-based
   std::vector<int> lw((size_t)p * q * S, -1);
   auto slot = [p, S](int r, int c, int s) { return ((size_t)c * p + r) * S + s; };
-  std::vector<int> panel_dev(tt.size(), -1);
+  // device tasks holding the reflectors (V, T) of each panel tile task
+  std::vector<std::vector<int>> panel_dev(tt.size());
   std::vector<int> dl;
   auto add = [&](DevTask t, std::vector<int> &d, int64_t prio) {
     std::sort(d.begin(), d.end());
@@ -132,53 +133,89 @@ void build_factor_graph(const std::vector<TileTask> &tt, const std::vector<int64
     key.emplace_back(prio, (int64_t)g.tasks.size());
     return (int)g.tasks.size() - 1;
   };
+  auto push_lw = [&](int r, int c, int s) { if (lw[slot(r, c, s)] >= 0) dl.push_back(lw[slot(r, c, s)]); };
   for (size_t x = 0; x < tt.size(); ++x) {
     const TileTask &t = tt[x];
     const int i = t.i - 1, pv = t.piv - 1, k = t.k - 1, j = t.j - 1;
     switch (t.kind) {
       case K_GEQRT: {
-        dl.clear();
-        for (int s = 0; s < S; ++s) if (lw[slot(i, k, s)] >= 0) dl.push_back(lw[slot(i, k, s)]);
-        int id = add(mk(K_GEQRT, i, 0, k, 0, 0), dl, start[x]);
-        for (int s = 0; s < S; ++s) lw[slot(i, k, s)] = id;
-        panel_dev[x] = id;
+        if (!split_panels) {
+          dl.clear();
+          for (int s = 0; s < S; ++s) push_lw(i, k, s);
+          int id = add(mk(K_GEQRT, i, 0, k, 0, 0), dl, start[x]);
+          for (int s = 0; s < S; ++s) lw[slot(i, k, s)] = id;
+          panel_dev[x].push_back(id);
+          break;
+        }
+        // left-looking emission: for each strip s, the updates by blocks < s, then its panel
+        std::vector<int> P(S, -1);
+        for (int s = 0; s < S; ++s) {
+          for (int b = 0; b < s; ++b) {
+            dl.clear();
+            dl.push_back(P[b]);
+            push_lw(i, k, s);
+            lw[slot(i, k, s)] = add(mk(K_GEQRT_U, i, 0, k, b, s), dl, start[x]);
+          }
+          dl.clear();
+          push_lw(i, k, s);
+          P[s] = add(mk(K_GEQRT_B, i, 0, k, 0, s), dl, start[x]);
+          lw[slot(i, k, s)] = P[s];
+        }
+        panel_dev[x] = P;
         break;
       }
       case K_TTQRT: case K_TSQRT: {
-        dl.clear();
-        for (int s = 0; s < S; ++s) {
-          if (lw[slot(pv, k, s)] >= 0) dl.push_back(lw[slot(pv, k, s)]);
-          if (lw[slot(i, k, s)] >= 0) dl.push_back(lw[slot(i, k, s)]);
+        if (!split_panels) {
+          dl.clear();
+          for (int s = 0; s < S; ++s) { push_lw(pv, k, s); push_lw(i, k, s); }
+          int id = add(mk(t.kind, i, pv, k, 0, 0), dl, start[x]);
+          for (int s = 0; s < S; ++s) lw[slot(pv, k, s)] = lw[slot(i, k, s)] = id;
+          panel_dev[x].push_back(id);
+          break;
         }
-        int id = add(mk(t.kind, i, pv, k, 0, 0), dl, start[x]);
-        for (int s = 0; s < S; ++s) lw[slot(pv, k, s)] = lw[slot(i, k, s)] = id;
-        panel_dev[x] = id;
+        const int kb = t.kind == K_TTQRT ? K_TTQRT_B : K_TSQRT_B;
+        const int ku = t.kind == K_TTQRT ? K_TTQRT_U : K_TSQRT_U;
+        std::vector<int> P(S, -1);
+        for (int s = 0; s < S; ++s) {
+          for (int b = 0; b < s; ++b) {
+            dl.clear();
+            dl.push_back(P[b]);
+            push_lw(pv, k, s);
+            push_lw(i, k, s);
+            int id = add(mk(ku, i, pv, k, b, s), dl, start[x]);
+            lw[slot(pv, k, s)] = lw[slot(i, k, s)] = id;
+          }
+          dl.clear();
+          push_lw(pv, k, s);
+          push_lw(i, k, s);
+          P[s] = add(mk(kb, i, pv, k, 0, s), dl, start[x]);
+          lw[slot(pv, k, s)] = lw[slot(i, k, s)] = P[s];
+        }
+        panel_dev[x] = P;
         break;
       }
       case K_UNMQR: {
         // the reflector source is the GEQRT of tile (i,k): the unique dep with kind GEQRT on (i,k)
-        int src = -1;
+        const std::vector<int> *src = nullptr;
         for (int d : t.deps)
-          if (tt[d].kind == K_GEQRT && tt[d].i == t.i && tt[d].k == t.k) src = panel_dev[d];
+          if (tt[d].kind == K_GEQRT && tt[d].i == t.i && tt[d].k == t.k) src = &panel_dev[d];
         for (int s = 0; s < S; ++s) {
-          dl.clear();
-          dl.push_back(src);
-          if (lw[slot(i, j, s)] >= 0) dl.push_back(lw[slot(i, j, s)]);
+          dl.assign(src->begin(), src->end());
+          push_lw(i, j, s);
           int id = add(mk(K_UNMQR, i, 0, k, j, s), dl, start[x]);
           lw[slot(i, j, s)] = id;
         }
         break;
       }
       case K_TTMQR: case K_TSMQR: {
-        int src = -1;
+        const std::vector<int> *src = nullptr;
         const int qk = t.kind == K_TTMQR ? K_TTQRT : K_TSQRT;
         for (int d : t.deps)
-          if (tt[d].kind == qk && tt[d].i == t.i && tt[d].k == t.k) src = panel_dev[d];
+          if (tt[d].kind == qk && tt[d].i == t.i && tt[d].k == t.k) src = &panel_dev[d];
         for (int s = 0; s < S; ++s) {
-          dl.clear();
-          dl.push_back(src);
-          if (lw[slot(pv, j, s)] >= 0) dl.push_back(lw[slot(pv, j, s)]);
-          if (lw[slot(i, j, s)] >= 0) dl.push_back(lw[slot(i, j, s)]);
+          dl.assign(src->begin(), src->end());
+          push_lw(pv, j, s);
+          push_lw(i, j, s);
           int id = add(mk(t.kind, i, pv, k, j, s), dl, start[x]);
           lw[slot(pv, j, s)] = lw[slot(i, j, s)] = id;
         }
@@ -230,6 +267,32 @@ void build_apply_graph(const std::vector<TileTask> &tt, int p, int qc, int nb, i
       }
   }
   reorder(g, key, deps);
+}
+
+void finalize_dataflow(DevGraph &g) {
+  const int n = (int)g.tasks.size();
+  std::vector<int32_t> cnt(n + 1, 0);
+  for (int t = 0; t < n; ++t)
+    for (int d = g.tasks[t].dep_begin; d < g.tasks[t].dep_end; ++d) ++cnt[g.deps[d] + 1];
+  for (int t = 0; t < n; ++t) cnt[t + 1] += cnt[t];
+  g.succ.assign(cnt[n], 0);
+  std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1);
+  g.roots.clear();
+  for (int t = 0; t < n; ++t) {
+    const DevTask &x = g.tasks[t];
+    for (int d = x.dep_begin; d < x.dep_end; ++d) g.succ[fill[g.deps[d]]++] = t;
+  }
+  for (int t = 0; t < n; ++t) {
+    DevTask &x = g.tasks[t];
+    const int indeg = x.dep_end - x.dep_begin;
+    const bool hi = x.kind == K_GEQRT || x.kind == K_TTQRT || x.kind == K_TSQRT || x.kind == K_GEQRT_B ||
+                    x.kind == K_TTQRT_B || x.kind == K_TSQRT_B ||
+                    ((x.kind == K_GEQRT_U || x.kind == K_TTQRT_U || x.kind == K_TSQRT_U) && x.s == x.j + 1);
+    x.meta = indeg | ((hi ? 1 : 0) << 16);
+    x.dep_begin = cnt[t];
+    x.dep_end = cnt[t + 1];
+    if (indeg == 0) g.roots.push_back(t);
+  }
 }
 
 }  // namespace tqr

@@ -14,7 +14,10 @@ struct Elim {            // elim(i, piv, k), 1-based (Algorithm 1, line
 enum Kind : int {
   K_GEQRT = 0, K_UNMQR = 1, K_TTQRT = 2, K_TTMQR = 3, K_TSQRT = 4, K_TSMQR = 5,
   // apply-only kinds (apply_qt / apply_q on a right-hand side C)
-  K_AP_UNMQR = 6, K_AP_TTMQR = 7, K_AP_TSMQR = 8
+  K_AP_UNMQR = 6, K_AP_TTMQR = 7, K_AP_TSMQR = 8,
+  // split panel kinds: one inner block b of a panel kernel (s = b), and the
+  // update of strip s of the same tile(s) by block b (j = b)
+  K_GEQRT_B = 9, K_GEQRT_U = 10, K_TTQRT_B = 11, K_TTQRT_U = 12, K_TSQRT_B = 13, K_TSQRT_U = 14
 };
 
 int kind_weight(int kind);   // Table 1 weights in units of nb^3/3
@@ -35,23 +38,35 @@ void expand(const std::vector<Elim> &lst, int p, int q, int family, std::vector<
 int64_t simulate(const std::vector<TileTask> &tasks, std::vector<int64_t> &start,
                  std::vector<int64_t> &finish);
 
-// Device task (16 bytes + dependency range). Shared layout with tiledqr.cu.
+// Device task record. Shared layout with tiledqr.cu / tqr_device.cuh.
+// Before finalize_dataflow: [dep_begin, dep_end) indexes DevGraph::deps.
+// After: [dep_begin, dep_end) indexes DevGraph::succ (successors) and
+// meta = indegree | (priority class << 16).
 struct DevTask {
   int16_t kind, i, piv, k, j, s;   // 0-based tile indices; s = column strip
-  int32_t dep_begin, dep_end;      // range in the dependency array
-  int32_t pad;
+  int32_t dep_begin, dep_end;
+  int32_t meta;
 };
 static_assert(sizeof(DevTask) == 24, "DevTask layout");
 
 struct DevGraph {
-  std::vector<DevTask> tasks;      // in execution priority order (topological)
+  std::vector<DevTask> tasks;      // in priority order (topological)
   std::vector<int32_t> deps;       // predecessor task ids (positions in `tasks`)
+  std::vector<int32_t> succ;       // successor task ids (after finalize_dataflow)
+  std::vector<int32_t> roots;      // tasks without predecessors, in priority order
 };
 
+// Convert the predecessor lists into successor lists, indegrees and the
+// priority class of every task (1 = panel chain: panel kernels and the
+// look-ahead strip update of split panels; 0 = other updates).
+void finalize_dataflow(DevGraph &g);
+
 // Strip-refined factorization graph: every update task is split into
-// ceil(nb/ws) column strips of width ws.
+// ceil(nb/ws) column strips of width ws; with split_panels (requires ws == ib)
+// every panel kernel becomes per-inner-block panel tasks plus trailing strip
+// tasks.
 void build_factor_graph(const std::vector<TileTask> &tt, const std::vector<int64_t> &start,
-                        int p, int q, int nb, int ws, DevGraph &g);
+                        int p, int q, int nb, int ws, bool split_panels, DevGraph &g);
 
 // Apply graph for C (p x qc tiles): Q^T (trans=1) or Q (trans=0).
 void build_apply_graph(const std::vector<TileTask> &tt, int p, int qc, int nb, int ws,

@@ -108,16 +108,19 @@ static int pick_ws(int nb, int ib) {
 // ---- plan cache -------------------------------------------------------------
 struct DevPlan {
   DevTask *tasks = nullptr;
-  int32_t *deps = nullptr;
-  int *done = nullptr;      // per-task completion epoch
-  int *ctrl = nullptr;      // [0] = next task, [1] = CTAs exited
-  unsigned long long *trace = nullptr;   // diagnostic per-task timestamps
-  std::vector<DevTask> host_tasks;      // kept for tqr_trace_fetch
-  int ntask = 0;
+  int32_t *succ = nullptr;
+  int32_t *roots = nullptr;
+  unsigned *cnt = nullptr;                // per-task arrivals (accumulate epoch x indegree)
+  unsigned long long *queue = nullptr;    // 2 x ntask ready-queue slots (epoch-tagged)
+  int *ctrl = nullptr;                    // scheduler counters (kCtrlWords ints)
+  unsigned long long *trace = nullptr;    // diagnostic per-task timestamps
+  std::vector<DevTask> host_tasks;        // kept for tqr_trace_fetch
+  int ntask = 0, nroots = 0;
   int epoch = 0;
   int ws = 0;
   ~DevPlan() {
-    cudaFree(tasks); cudaFree(deps); cudaFree(done); cudaFree(ctrl); cudaFree(trace);
+    cudaFree(tasks); cudaFree(succ); cudaFree(roots); cudaFree(cnt); cudaFree(queue); cudaFree(ctrl);
+    cudaFree(trace);
   }
 };
 
@@ -127,18 +130,22 @@ static std::map<PlanKey, std::unique_ptr<DevPlan>> g_plans;
 
 static int upload(const DevGraph &g, int ws, DevPlan &pl) {
   pl.ntask = (int)g.tasks.size();
+  pl.nroots = (int)g.roots.size();
   pl.host_tasks = g.tasks;
   pl.ws = ws;
-  size_t tb = sizeof(DevTask) * (g.tasks.size() ? g.tasks.size() : 1);
-  size_t db = sizeof(int32_t) * (g.deps.size() ? g.deps.size() : 1);
-  CUDA_TRY(cudaMalloc(&pl.tasks, tb));
-  CUDA_TRY(cudaMalloc(&pl.deps, db));
-  CUDA_TRY(cudaMalloc(&pl.done, sizeof(int) * (pl.ntask ? pl.ntask : 1)));
-  CUDA_TRY(cudaMalloc(&pl.ctrl, sizeof(int) * 4));
+  const size_t n1 = pl.ntask ? pl.ntask : 1;
+  CUDA_TRY(cudaMalloc(&pl.tasks, sizeof(DevTask) * n1));
+  CUDA_TRY(cudaMalloc(&pl.succ, sizeof(int32_t) * (g.succ.empty() ? 1 : g.succ.size())));
+  CUDA_TRY(cudaMalloc(&pl.roots, sizeof(int32_t) * (g.roots.empty() ? 1 : g.roots.size())));
+  CUDA_TRY(cudaMalloc(&pl.cnt, sizeof(unsigned) * n1));
+  CUDA_TRY(cudaMalloc(&pl.queue, sizeof(unsigned long long) * 2 * n1));
+  CUDA_TRY(cudaMalloc(&pl.ctrl, sizeof(int) * kCtrlWords));
   if (!g.tasks.empty()) CUDA_TRY(cudaMemcpy(pl.tasks, g.tasks.data(), sizeof(DevTask) * g.tasks.size(), cudaMemcpyHostToDevice));
-  if (!g.deps.empty()) CUDA_TRY(cudaMemcpy(pl.deps, g.deps.data(), sizeof(int32_t) * g.deps.size(), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemset(pl.done, 0, sizeof(int) * (pl.ntask ? pl.ntask : 1)));
-  CUDA_TRY(cudaMemset(pl.ctrl, 0, sizeof(int) * 4));
+  if (!g.succ.empty()) CUDA_TRY(cudaMemcpy(pl.succ, g.succ.data(), sizeof(int32_t) * g.succ.size(), cudaMemcpyHostToDevice));
+  if (!g.roots.empty()) CUDA_TRY(cudaMemcpy(pl.roots, g.roots.data(), sizeof(int32_t) * g.roots.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemset(pl.cnt, 0, sizeof(unsigned) * n1));
+  CUDA_TRY(cudaMemset(pl.queue, 0, sizeof(unsigned long long) * 2 * n1));
+  CUDA_TRY(cudaMemset(pl.ctrl, 0, sizeof(int) * kCtrlWords));
   return 0;
 }
 
@@ -148,7 +155,7 @@ static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, in
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   int ws = pick_ws(nb, ib);
-  PlanKey key{dev, mode, p, q, qc, nb, ib, tree, bs, family, ws};
+  PlanKey key{dev, mode, p, q, qc, nb, ib, tree, bs, family, ws * 2 + (env_int("TQR_SPLIT", 1) != 0)};
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_plans.find(key);
   if (it != g_plans.end()) { *out = it->second.get(); return 0; }
@@ -158,8 +165,10 @@ static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, in
   int rc = tile_sim(p, q, tree, bs, family, tt, st, fin, mk);
   if (rc < 0) return rc;
   DevGraph g;
-  if (mode == 0) build_factor_graph(tt, st, p, q, nb, ws, g);
+  const bool split = env_int("TQR_SPLIT", 1) != 0 && ws == ib && nb > ib;
+  if (mode == 0) build_factor_graph(tt, st, p, q, nb, ws, split, g);
   else build_apply_graph(tt, p, qc, nb, ws, mode == 1, g);
+  finalize_dataflow(g);
   auto pl = std::make_unique<DevPlan>();
   rc = upload(g, ws, *pl);
   if (rc < 0) return rc;
@@ -227,8 +236,8 @@ static int launch(DevPlan *pl, int p, int q, int nb, int ib, double *A, double *
     attr_set_dev = dev;
   }
   RunArgs a;
-  a.tasks = pl->tasks; a.deps = pl->deps; a.ntask = pl->ntask;
-  a.done = pl->done; a.ctrl = pl->ctrl; a.epoch = ++pl->epoch;
+  a.tasks = pl->tasks; a.succ = pl->succ; a.roots = pl->roots; a.nroots = pl->nroots; a.ntask = pl->ntask;
+  a.cnt = pl->cnt; a.queue = pl->queue; a.ctrl = pl->ctrl; a.epoch = ++pl->epoch;
   a.A = A; a.T = T; a.C = C;
   a.p = p; a.q = q; a.nb = nb; a.ib = ib; a.ws = pl->ws; a.trans = trans;
   a.trace = nullptr;

@@ -20,15 +20,20 @@ constexpr int kMaxNb = 256;
 constexpr int kMaxIb = 32;
 constexpr size_t kMaxSmem = 227 * 1024 - 512;   // dynamic smem budget (opt-in max minus static)
 constexpr int kTld = 33;
-constexpr int kTraceWords = 12;             // per-task trace record (diagnostics)                    // ld of the 32 x 32 smem T / top / G blocks
+constexpr int kTraceWords = 12;             // per-task trace record (diagnostics)
+// scheduler control words (ints; each on its own 128-byte line)
+constexpr int kCtrlHead = 0, kCtrlTail = 32, kCtrlDone = 128, kCtrlExit = 160, kCtrlWords = 192;                    // ld of the 32 x 32 smem T / top / G blocks
 constexpr int kPanelScratch = 2 * 32 * kTld + 2 * 256 + 8 + 32;
 
 struct RunArgs {
   const DevTask *tasks;
-  const int32_t *deps;
+  const int32_t *succ;          // successor lists (CSR, ranges in the task records)
+  const int32_t *roots;         // tasks without predecessors
+  int nroots;
   int ntask;
-  int *done;     // per-task completion epoch
-  int *ctrl;     // [0] next task, [1] exited CTAs
+  unsigned *cnt;                // per-task arrivals, accumulated over launches (epoch * indegree when ready)
+  unsigned long long *queue;    // 2 ready queues of ntask slots: [0..ntask) panel chain, [ntask..2 ntask) others
+  int *ctrl;                    // kCtrl* counters
   int epoch;
   int nctas;
   double *A, *T, *C;
@@ -651,14 +656,15 @@ __device__ void panel_task(double *X, double *A1, double *Tslot, int nb, int ib,
 }
 
 // ---- update kernels on one column strip -----------------------------------
-// UNMQR: C (tile strip) <- Q^T C with the GEQRT reflectors of tile Vt
+// UNMQR: C (tile strip) <- Q^T C (or Q C) with inner blocks [b_lo, b_hi) of the
+// GEQRT reflectors of tile Vt; only rows >= b_lo*ib are touched.
 __device__ void unmqr_strip(const double *Vt, const double *Tslot, double *Ct, int nb, int ib, int cs,
-                            int wsz, bool trans, double *smem, const SmemLayout &L) {
+                            int wsz, bool trans, int b_lo, int b_hi, double *smem, const SmemLayout &L) {
   double *Cb = smem + L.offC, *Vb = smem + L.offV, *Wb = smem + L.offW, *Ts = smem + L.offT;
-  load_rows(Cb, L.ldc, 0, Ct, nb, 0, nb, cs, wsz);
-  const int nblk = (nb + ib - 1) / ib;
-  for (int t = 0; t < nblk; ++t) {
-    const int b = trans ? t : nblk - 1 - t;
+  const int r0 = b_lo * ib;
+  load_rows(Cb, L.ldc, 0, Ct, nb, r0, nb, cs, wsz);
+  for (int t = b_lo; t < b_hi; ++t) {
+    const int b = trans ? t : b_hi - 1 - (t - b_lo);
     const int j0 = b * ib, bw = min(ib, nb - j0);
     issue_v_geqrt(Vb, L.ldv, Vt, nb, j0, bw);
     issue_t(Ts, Tslot, ib, j0, bw);
@@ -670,18 +676,21 @@ __device__ void unmqr_strip(const double *Vt, const double *Tslot, double *Ct, i
     prof_mark(PH_FIX);
     apply_block(nullptr, Cb + j0, L.ldc, nb - j0, Vb, L.ldv, Ts, bw, wsz, trans, Wb, Wb + L.ldw * L.wcols);
   }
-  store_rows(Cb, L.ldc, 0, Ct, nb, 0, nb, cs, wsz);
+  store_rows(Cb, L.ldc, 0, Ct, nb, r0, nb, cs, wsz);
 }
 
-// TTMQR / TSMQR: [C1; C2] <- Q^T [C1; C2] with the TTQRT/TSQRT reflectors V2 of tile Vt
+// TTMQR / TSMQR: [C1; C2] <- Q^T [C1; C2] (or Q) with inner blocks [b_lo, b_hi)
+// of the TTQRT/TSQRT reflectors V2 of tile Vt. Block b touches C1 rows
+// b*ib .. b*ib+bw-1 and C2 rows 0 .. (tri ? b*ib+bw : nb)-1.
 __device__ void tpmqr_strip(const double *Vt, const double *Tslot, double *C1, double *C2, int nb, int ib,
-                            int cs, int wsz, bool tri, bool trans, double *smem, const SmemLayout &L) {
+                            int cs, int wsz, bool tri, bool trans, int b_lo, int b_hi, double *smem,
+                            const SmemLayout &L) {
   double *Cb = smem + L.offC, *Vb = smem + L.offV, *Wb = smem + L.offW, *Ts = smem + L.offT;
-  load_rows(Cb, L.ldc, 0, C1, nb, 0, nb, cs, wsz);
-  load_rows(Cb, L.ldc, nb, C2, nb, 0, nb, cs, wsz);
-  const int nblk = (nb + ib - 1) / ib;
-  for (int t = 0; t < nblk; ++t) {
-    const int b = trans ? t : nblk - 1 - t;
+  const int r1lo = b_lo * ib, r1hi = min(b_hi * ib, nb), r2hi = tri ? r1hi : nb;
+  load_rows(Cb, L.ldc, 0, C1, nb, r1lo, r1hi, cs, wsz);
+  load_rows(Cb, L.ldc, nb, C2, nb, 0, r2hi, cs, wsz);
+  for (int t = b_lo; t < b_hi; ++t) {
+    const int b = trans ? t : b_hi - 1 - (t - b_lo);
     const int j0 = b * ib, bw = min(ib, nb - j0);
     issue_v_tp(Vb, L.ldv, Vt, nb, j0, bw, tri);
     issue_t(Ts, Tslot, ib, j0, bw);
@@ -693,12 +702,14 @@ __device__ void tpmqr_strip(const double *Vt, const double *Tslot, double *C1, d
     prof_mark(PH_FIX);
     apply_block(Cb + j0, Cb + nb, L.ldc, tri ? j0 + bw : nb, Vb, L.ldv, Ts, bw, wsz, trans, Wb, Wb + L.ldw * L.wcols);
   }
-  store_rows(Cb, L.ldc, 0, C1, nb, 0, nb, cs, wsz);
-  store_rows(Cb, L.ldc, nb, C2, nb, 0, nb, cs, wsz);
+  store_rows(Cb, L.ldc, 0, C1, nb, r1lo, r1hi, cs, wsz);
+  store_rows(Cb, L.ldc, nb, C2, nb, 0, r2hi, cs, wsz);
 }
 
 __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const SmemLayout &L) {
   const int p = a.p, nb = a.nb, ib = a.ib, ws = a.ws;
+  const int nblk = (nb + ib - 1) / ib;
+  double *Vb = smem + L.offV, *Wb = smem + L.offW, *Ts = smem + L.offT;
   switch (t.kind) {
     case K_GEQRT:
       panel_task<0>(tile_ptr(a.A, p, nb, t.i, t.k), nullptr, tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0), nb, ib, ws,
@@ -712,12 +723,43 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
       panel_task<2>(tile_ptr(a.A, p, nb, t.i, t.k), tile_ptr(a.A, p, nb, t.piv, t.k),
                     tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1), nb, ib, ws, smem, L);
       break;
+    // ---- split panels: inner block s of the panel, or update of strip s by block j
+    case K_GEQRT_B: {
+      const int j0 = t.s * ib;
+      panel_block<0>(tile_ptr(a.A, p, nb, t.i, t.k), nullptr, tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0), nb, ib, j0,
+                     min(ib, nb - j0), Vb, L.ldv, Ts, Wb);
+      break;
+    }
+    case K_TTQRT_B:
+    case K_TSQRT_B: {
+      const int j0 = t.s * ib;
+      double *X = tile_ptr(a.A, p, nb, t.i, t.k), *A1 = tile_ptr(a.A, p, nb, t.piv, t.k);
+      double *Tsl = tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1);
+      if (t.kind == K_TTQRT_B) panel_block<1>(X, A1, Tsl, nb, ib, j0, min(ib, nb - j0), Vb, L.ldv, Ts, Wb);
+      else panel_block<2>(X, A1, Tsl, nb, ib, j0, min(ib, nb - j0), Vb, L.ldv, Ts, Wb);
+      break;
+    }
+    case K_GEQRT_U: {
+      const int cs = t.s * ws, wsz = min(ws, nb - cs);
+      double *X = tile_ptr(a.A, p, nb, t.i, t.k);
+      unmqr_strip(X, tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0), X, nb, ib, cs, wsz, true, t.j, t.j + 1, smem, L);
+      break;
+    }
+    case K_TTQRT_U:
+    case K_TSQRT_U: {
+      const int cs = t.s * ws, wsz = min(ws, nb - cs);
+      double *X = tile_ptr(a.A, p, nb, t.i, t.k);
+      tpmqr_strip(X, tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1), tile_ptr(a.A, p, nb, t.piv, t.k), X, nb, ib, cs, wsz,
+                  t.kind == K_TTQRT_U, true, t.j, t.j + 1, smem, L);
+      break;
+    }
+    // ---- updates of other tiles (factorization) and of C (apply)
     case K_UNMQR:
     case K_AP_UNMQR: {
       double *Cbase = t.kind == K_UNMQR ? a.A : a.C;
       const int cs = t.s * ws, wsz = min(ws, nb - cs);
       unmqr_strip(tile_ptr(a.A, p, nb, t.i, t.k), tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0),
-                  tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs, wsz, a.trans != 0, smem, L);
+                  tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs, wsz, a.trans != 0, 0, nblk, smem, L);
       break;
     }
     case K_TTMQR:
@@ -730,7 +772,7 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
       const int cs = t.s * ws, wsz = min(ws, nb - cs);
       tpmqr_strip(tile_ptr(a.A, p, nb, t.i, t.k), tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1),
                   tile_ptr(Cbase, p, nb, t.piv, t.j), tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs, wsz, tri,
-                  a.trans != 0, smem, L);
+                  a.trans != 0, 0, nblk, smem, L);
       break;
     }
     default:
@@ -739,10 +781,57 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
 }
 
 // ---- the persistent dataflow kernel ----------------------------------------
-// Tasks are taken in the host's topological priority order through one global
-// counter; a task waits on the completion flags of its predecessors (all of
-// which were taken earlier by running CTAs, so the wait always ends), runs on
-// the whole CTA, then publishes its own flag (release / acquire at gpu scope).
+// Dataflow with per-task dependency counters (north_star: "a persistent kernel
+// gated by per-tile dependency counters"). A finished task bumps the counter
+// of each successor (atom.acq_rel); the predecessor that completes a
+// successor's count pushes it on one of two ready queues (panel chain first).
+// CTAs only ever take ready tasks, so no CTA idles on a specific task while
+// others are runnable. Queue slots carry the launch epoch, counters
+// accumulate epoch x indegree, and the last CTA to leave resets the queue
+// heads/tails: nothing is cleared between launches (one launch per call).
+__device__ __forceinline__ unsigned atom_add_acqrel(unsigned *p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ int ld_relaxed(const int *p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void push_ready(const RunArgs &a, int t) {
+  const int q = (a.tasks[t].meta >> 16) & 1 ? 0 : 1;     // 0 = panel chain queue
+  const int pos = atomicAdd(&a.ctrl[kCtrlTail + 8 * q], 1);
+  st_release64(a.queue + (size_t)q * a.ntask + pos, ((unsigned long long)(unsigned)a.epoch << 32) | (unsigned)t);
+}
+
+// claim the next slot of queue q if one is published; returns the task or -1
+__device__ __forceinline__ int try_pop(const RunArgs &a, int q) {
+  int *head = &a.ctrl[kCtrlHead + 8 * q];
+  const int *tail = &a.ctrl[kCtrlTail + 8 * q];
+  int h = ld_relaxed(head);
+  while (h < ld_relaxed(tail)) {
+    const int got = atomicCAS(head, h, h + 1);
+    if (got == h) {
+      const unsigned long long *slot = a.queue + (size_t)q * a.ntask + h;
+      unsigned long long v;
+      while (((v = ld_acquire64(slot)) >> 32) != (unsigned)a.epoch) __nanosleep(20);
+      return (int)(v & 0xffffffffu);
+    }
+    h = got;
+  }
+  return -1;
+}
+
 __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_task;
@@ -750,45 +839,59 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
   if (threadIdx.x == 0) s_prof_on = 0;
   // everything the DMMA padding may read must be finite: start from zeros
   for (size_t x = threadIdx.x; x < L.total; x += kThreads) smem[x] = 0.0;
+  if (threadIdx.x == 0)
+    for (int r = blockIdx.x; r < a.nroots; r += gridDim.x) push_ready(a, a.roots[r]);
   for (;;) {
-    if (threadIdx.x == 0) s_task = atomicAdd(&a.ctrl[0], 1);
+    if (threadIdx.x == 0) {
+      unsigned long long t_take = a.trace ? globaltimer() : 0ull;
+      int t;
+      for (;;) {
+        if (ld_relaxed(&a.ctrl[kCtrlDone]) >= a.ntask) { t = -1; break; }
+        t = try_pop(a, 0);
+        if (t >= 0) break;
+        t = try_pop(a, 1);
+        if (t >= 0) break;
+        __nanosleep(64);
+      }
+      s_task = t;
+      if (a.trace && t >= 0) {
+        a.trace[kTraceWords * (size_t)t] = t_take;
+        a.trace[kTraceWords * (size_t)t + 1] = globaltimer();
+        for (int x = 0; x < 8; ++x) s_prof[x] = 0;
+        s_prof_last = clock64();
+        s_prof_on = 1;
+      }
+    }
     __syncthreads();
     const int t = s_task;
-    if (t >= a.ntask) break;
-    const DevTask tk = a.tasks[t];
-    unsigned long long t_take = 0, t_ready = 0;
-    if (a.trace && threadIdx.x == 0) t_take = globaltimer();
-    for (int d = tk.dep_begin + threadIdx.x; d < tk.dep_end; d += kThreads) {
-      const int *f = a.done + a.deps[d];
-      while (ld_acquire(f) != a.epoch) __nanosleep(32);
-    }
+    if (t < 0) break;
     __threadfence();
-    __syncthreads();
-    if (a.trace && threadIdx.x == 0) {
-      t_ready = globaltimer();
-      for (int x = 0; x < 8; ++x) s_prof[x] = 0;
-      s_prof_last = clock64();
-      s_prof_on = 1;
-    }
+    const DevTask tk = a.tasks[t];
     run_task(a, tk, smem, L);
     __syncthreads();
     prof_mark(PH_STORE);
     if (threadIdx.x == 0) {
       __threadfence();
-      st_release(a.done + t, a.epoch);
+      for (int x = tk.dep_begin; x < tk.dep_end; ++x) {
+        const int sc = a.succ[x];
+        const unsigned need = (unsigned)a.epoch * (unsigned)(a.tasks[sc].meta & 0xffff);
+        if (atom_add_acqrel(a.cnt + sc, 1u) + 1u == need) push_ready(a, sc);
+      }
       if (a.trace) {
         unsigned long long *tr = a.trace + kTraceWords * (size_t)t;
-        tr[0] = t_take; tr[1] = t_ready; tr[2] = globaltimer();
+        tr[2] = globaltimer();
         tr[3] = ((unsigned long long)smid() << 32) | (unsigned)tk.kind;
         for (int x = 0; x < 8; ++x) tr[4 + x] = s_prof[x];
       }
+      atomicAdd(&a.ctrl[kCtrlDone], 1);
     }
   }
   if (threadIdx.x == 0) {
-    const int n = atomicAdd(&a.ctrl[1], 1);
+    const int n = atomicAdd(&a.ctrl[kCtrlExit], 1);
     if (n == a.nctas - 1) {
-      a.ctrl[0] = 0;
-      a.ctrl[1] = 0;
+      a.ctrl[kCtrlHead] = 0; a.ctrl[kCtrlTail] = 0;
+      a.ctrl[kCtrlHead + 8] = 0; a.ctrl[kCtrlTail + 8] = 0;
+      a.ctrl[kCtrlDone] = 0; a.ctrl[kCtrlExit] = 0;
       __threadfence();
     }
   }

@@ -69,6 +69,9 @@ CASES = [
     (5, 5, 12, 5),
     (7, 2, 24, 32),
     (4, 1, 16, 16),
+    # nb > ws = ib = 32: panels split into per-inner-block tasks (+ ragged last block)
+    (4, 2, 72, 32),
+    (3, 3, 64, 32),
 ]
 TREES = [("flat", 1), ("fibonacci", 1), ("greedy", 1), ("binary", 1), ("plasma", 2), ("plasma", 3)]
 
@@ -81,6 +84,15 @@ def test_factor_parity_small(tree, bs, family):
             continue
         A = qrinputs.gaussian(p * nb, q * nb, 1000 + 7 * p + q)
         compare_with_oracle(A, nb, ib, tree, bs, family)
+
+
+@pytest.mark.parametrize("tree,family", [("greedy", "TT"), ("flat", "TS"), ("plasma", "TT")])
+def test_monolithic_panels_match(tree, family, monkeypatch):
+    """TQR_SPLIT=0 runs every panel kernel as one task; results equal the oracle too."""
+    monkeypatch.setenv("TQR_SPLIT", "0")
+    for (p, q, nb, ib) in [(4, 2, 72, 32), (3, 3, 64, 32)]:
+        A = qrinputs.gaussian(p * nb, q * nb, 77 + p)
+        compare_with_oracle(A, nb, ib, tree, 2 if tree == "plasma" else 1, family)
 
 
 def test_config0_greedy_full_checks():
