@@ -96,6 +96,7 @@ void reorder(DevGraph &g, const std::vector<std::pair<int64_t, int64_t>> &key,
   g.deps.clear();
   for (int r = 0; r < n; ++r) {
     DevTask t = g.tasks[ord[r]];
+    if (t.chain >= 0) t.chain = pos[t.chain];
     t.dep_begin = (int32_t)g.deps.size();
     for (int d : deps[ord[r]]) g.deps.push_back(pos[d]);
     t.dep_end = (int32_t)g.deps.size();
@@ -107,7 +108,7 @@ void reorder(DevGraph &g, const std::vector<std::pair<int64_t, int64_t>> &key,
 DevTask mk(int kind, int i, int piv, int k, int j, int s) {
   DevTask t;
   t.kind = (int16_t)kind; t.i = (int16_t)i; t.piv = (int16_t)piv; t.k = (int16_t)k;
-  t.j = (int16_t)j; t.s = (int16_t)s; t.dep_begin = t.dep_end = 0; t.meta = 0;
+  t.j = (int16_t)j; t.s = (int16_t)s; t.dep_begin = t.dep_end = 0; t.meta = 0; t.chain = -1; t.pad = 0;
   return t;
 }
 
@@ -154,11 +155,14 @@ void build_factor_graph(const std::vector<TileTask> &tt, const std::vector<int64
             dl.clear();
             dl.push_back(P[b]);
             push_lw(i, k, s);
-            lw[slot(i, k, s)] = add(mk(K_GEQRT_U, i, 0, k, b, s), dl, start[x]);
+            const int u = add(mk(K_GEQRT_U, i, 0, k, b, s), dl, start[x]);
+            lw[slot(i, k, s)] = u;
+            if (b == s - 1) g.tasks[P[b]].chain = u;          // P(b) -> U(b, b+1)
           }
           dl.clear();
           push_lw(i, k, s);
           P[s] = add(mk(K_GEQRT_B, i, 0, k, 0, s), dl, start[x]);
+          if (s > 0) g.tasks[lw[slot(i, k, s)]].chain = P[s];  // U(s-1, s) -> P(s)
           lw[slot(i, k, s)] = P[s];
         }
         panel_dev[x] = P;
@@ -184,11 +188,13 @@ void build_factor_graph(const std::vector<TileTask> &tt, const std::vector<int64
             push_lw(i, k, s);
             int id = add(mk(ku, i, pv, k, b, s), dl, start[x]);
             lw[slot(pv, k, s)] = lw[slot(i, k, s)] = id;
+            if (b == s - 1) g.tasks[P[b]].chain = id;         // P(b) -> U(b, b+1)
           }
           dl.clear();
           push_lw(pv, k, s);
           push_lw(i, k, s);
           P[s] = add(mk(kb, i, pv, k, 0, s), dl, start[x]);
+          if (s > 0) g.tasks[lw[slot(i, k, s)]].chain = P[s];  // U(s-1, s) -> P(s)
           lw[slot(pv, k, s)] = lw[slot(i, k, s)] = P[s];
         }
         panel_dev[x] = P;
@@ -282,13 +288,16 @@ void finalize_dataflow(DevGraph &g) {
     const DevTask &x = g.tasks[t];
     for (int d = x.dep_begin; d < x.dep_end; ++d) g.succ[fill[g.deps[d]]++] = t;
   }
+  std::vector<char> chained(n, 0);
+  for (int t = 0; t < n; ++t)
+    if (g.tasks[t].chain >= 0) chained[g.tasks[t].chain] = 1;
   for (int t = 0; t < n; ++t) {
     DevTask &x = g.tasks[t];
     const int indeg = x.dep_end - x.dep_begin;
     const bool hi = x.kind == K_GEQRT || x.kind == K_TTQRT || x.kind == K_TSQRT || x.kind == K_GEQRT_B ||
                     x.kind == K_TTQRT_B || x.kind == K_TSQRT_B ||
                     ((x.kind == K_GEQRT_U || x.kind == K_TTQRT_U || x.kind == K_TSQRT_U) && x.s == x.j + 1);
-    x.meta = indeg | ((hi ? 1 : 0) << 16);
+    x.meta = indeg | ((hi ? 1 : 0) << 16) | (chained[t] ? 1 << 17 : 0);
     x.dep_begin = cnt[t];
     x.dep_end = cnt[t + 1];
     if (indeg == 0) g.roots.push_back(t);

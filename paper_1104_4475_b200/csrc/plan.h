@@ -42,12 +42,16 @@ int64_t simulate(const std::vector<TileTask> &tasks, std::vector<int64_t> &start
 // Before finalize_dataflow: [dep_begin, dep_end) indexes DevGraph::deps.
 // After: [dep_begin, dep_end) indexes DevGraph::succ (successors) and
 // meta = indegree | (priority class << 16).
+// chain = a successor the same CTA runs next when it is ready (panel chain of
+// split panels: P(b) -> U(b,b+1) -> P(b+1)), -1 if none.
 struct DevTask {
   int16_t kind, i, piv, k, j, s;   // 0-based tile indices; s = column strip
   int32_t dep_begin, dep_end;
   int32_t meta;
+  int32_t chain;
+  int32_t pad;
 };
-static_assert(sizeof(DevTask) == 24, "DevTask layout");
+static_assert(sizeof(DevTask) == 32, "DevTask layout");
 
 struct DevGraph {
   std::vector<DevTask> tasks;      // in priority order (topological)
@@ -58,7 +62,8 @@ struct DevGraph {
 
 // Convert the predecessor lists into successor lists, indegrees and the
 // priority class of every task (1 = panel chain: panel kernels and the
-// look-ahead strip update of split panels; 0 = other updates).
+// look-ahead strip update of split panels; 0 = other updates); chain targets
+// get meta bit 17 (one virtual extra dependency held by the chain owner).
 void finalize_dataflow(DevGraph &g);
 
 // Strip-refined factorization graph: every update task is split into

@@ -42,8 +42,8 @@ struct RunArgs {
 };
 
 struct SmemLayout {
-  int ldc, ldv, ldw, wcols;
-  size_t offC, offV, offW, offT, total;   // in doubles
+  int ldc, ldv, ldw, wcols, nvb;
+  size_t offC, offV[2], offW, offT[2], total;   // in doubles
 };
 
 // Leading dimensions are = 4 (mod 16) doubles: the DMMA fragment loads of a
@@ -52,21 +52,31 @@ struct SmemLayout {
 __host__ __device__ inline int ld4(int n) { return n + ((4 - n % 16) + 16) % 16; }
 __host__ __device__ inline int round_up(int n, int m) { return (n + m - 1) / m * m; }
 
+// C buffer rows: single-tile strips (UNMQR, GEQRT trailing) use rows 0..nb-1;
+// two-tile strips (TTMQR/TSMQR) keep C2 at rows kWinRows.. and stream the 32
+// C1 rows of each inner block through two windows at rows 0 and 32.
+constexpr int kWinRows = 64;
+
 __host__ __device__ inline SmemLayout smem_layout(int nb, int ib, int ws) {
   SmemLayout s;
   s.wcols = round_up(ws, 8);
-  s.ldc = ld4(2 * nb + 16);          // [C1 rows 0..nb-1 | C2 rows nb..2nb-1 | m16 padding]
-  s.ldv = ld4(round_up(nb, 16));     // V rows incl. m16 / k4 padding
+  s.ldc = ld4(nb + kWinRows + 16);
+  s.ldv = ld4(round_up(nb, 16));
   s.ldw = 36;
-  size_t c = (size_t)s.ldc * s.wcols;
-  size_t v = (size_t)s.ldv * 32;
+  const size_t c = (size_t)s.ldc * s.wcols;
+  const size_t v = (size_t)s.ldv * 32;
   size_t w = (size_t)2 * s.ldw * s.wcols;
   if (w < (size_t)kPanelScratch) w = kPanelScratch;
+  const size_t tt = 32 * kTld;
+  s.nvb = (c + 2 * v + w + 2 * tt) * sizeof(double) <= kMaxSmem ? 2 : 1;   // double-buffer V/T if it fits
   s.offC = 0;
-  s.offV = c;
-  s.offW = c + v;
-  s.offT = c + v + w;
-  s.total = s.offT + 32 * kTld;
+  s.offV[0] = c;
+  s.offV[1] = c + v;
+  s.offW = c + s.nvb * v;
+  s.offT[0] = s.offW + w;
+  s.offT[1] = s.offT[0] + tt;
+  s.total = s.offT[0] + s.nvb * tt;
+  if (s.nvb == 1) { s.offV[1] = s.offV[0]; s.offT[1] = s.offT[0]; }
   return s;
 }
 
@@ -244,33 +254,45 @@ __device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, doubl
 // V = [I; V2] (TT/TS kernels). All arrays in smem, column-major.
 // Requirements (kept by the loaders): V rows [nrows, round_up(nrows,4)) are
 // zero; everything the m16/n8 padding reads is finite; W/W2 have ldw = 36.
-// Both contractions run on the FP64 tensor pipe (mma.sync m16n8k4 f64).
-__device__ void apply_block(double *Ctop, double *Cv, int ldc, int nrows, const double *V, int ldv,
-                            const double *Ts, int bw, int wsz, bool trans, double *W, double *W2) {
+// All three contractions run on the FP64 tensor pipe (mma.sync m16n8k4 f64).
+// DMMA latency (~150 cycles) is hidden with several independent accumulator
+// chains per warp: K is interleaved over 4 chains in phase 1 and 2 chains in
+// phase 2, and phase 3 deals the (m16, n8) fragments round-robin over warps
+// (warp w: n-tile w mod NT, m-tiles w / NT + i * 8 / NT).
+template <int NT>
+__device__ void apply_block_t(double *Ctop, double *Cv, int ldc, int nrows, const double *V, int ldv,
+                              const double *Ts, int bw, int wsz, bool trans, double *W, double *W2) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   constexpr int ldw = 36;
-  // phase 1: W (bw x wsz) = V^T Cv, one 16x8 fragment per warp-iteration, full K
+  const int nt = (wsz + 7) >> 3;
+  // phase 1: W (bw x wsz) = V^T Cv, one 16x8 fragment per warp-iteration, full K in 4 chains
   {
-    const int mt = (bw + 15) >> 4, nt = (wsz + 7) >> 3;
+    const int mt = (bw + 15) >> 4;
     const int kpad = (nrows + 3) & ~3;
     for (int f = warp; f < mt * nt; f += kWarps) {
       const int m0 = (f % mt) * 16, n0 = (f / mt) * 8;
-      double acc0[4] = {0.0, 0.0, 0.0, 0.0}, acc1[4] = {0.0, 0.0, 0.0, 0.0};
+      double acc[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[u][e] = 0.0;
       const double *va = V + (m0 + g) * ldv + t;
       const double *vb = va + 8 * ldv;
       const double *cb = Cv + (n0 + g) * ldc + t;
       int k = 0;
-      for (; k + 8 <= kpad; k += 8) {
-        dmma(acc0, va[k], vb[k], cb[k]);
-        dmma(acc1, va[k + 4], vb[k + 4], cb[k + 4]);
+      for (; k + 16 <= kpad; k += 16) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma(acc[u], va[k + 4 * u], vb[k + 4 * u], cb[k + 4 * u]);
       }
-      if (k < kpad) dmma(acc0, va[k], vb[k], cb[k]);
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+        if (k + 4 * u < kpad) dmma(acc[u], va[k + 4 * u], vb[k + 4 * u], cb[k + 4 * u]);
       const int r0 = m0 + g, c0 = n0 + 2 * t;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int r = r0 + (e >> 1) * 8, c = c0 + (e & 1);
-        double v = acc0[e] + acc1[e];
+        double v = (acc[0][e] + acc[1][e]) + (acc[2][e] + acc[3][e]);
         if (Ctop && r < bw && c < wsz) v += Ctop[r + c * ldc];
         W[r + c * ldw] = v;
       }
@@ -281,73 +303,74 @@ __device__ void apply_block(double *Ctop, double *Cv, int ldc, int nrows, const 
   // phase 2: W2 = -op(T) W on the tensor pipe (T is a zero-padded 32 x 32
   // upper triangle, so rows bw..31 of W2 come out exactly zero)
   const int kpad3 = (bw + 3) & ~3;
-  {
-    const int nt = (wsz + 7) >> 3;
-    for (int f = warp; f < 2 * nt; f += kWarps) {
-      const int m0 = (f & 1) * 16, n0 = (f >> 1) * 8;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int k = 0; k < kpad3; k += 4) {
-        double a0, a1;
-        if (trans) {   // A[l][m] = T[m][l]
-          a0 = Ts[(k + t) + (m0 + g) * kTld];
-          a1 = Ts[(k + t) + (m0 + g + 8) * kTld];
-        } else {       // A[l][m] = T[l][m]
-          a0 = Ts[(m0 + g) + (k + t) * kTld];
-          a1 = Ts[(m0 + g + 8) + (k + t) * kTld];
-        }
-        dmma(acc, a0, a1, W[(k + t) + (n0 + g) * ldw]);
-      }
+  for (int f = warp; f < 2 * nt; f += kWarps) {
+    const int m0 = (f & 1) * 16, n0 = (f >> 1) * 8;
+    double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+    for (int k = 0; k < kpad3; k += 8) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int r = m0 + g + (e >> 1) * 8, c = n0 + 2 * t + (e & 1);
-        W2[r + c * ldw] = -acc[e];
+      for (int u = 0; u < 2; ++u) {
+        const int kk = k + 4 * u;
+        if (kk < kpad3) {
+          double a0, a1;
+          if (trans) {   // A[l][m] = T[m][l]
+            a0 = Ts[(kk + t) + (m0 + g) * kTld];
+            a1 = Ts[(kk + t) + (m0 + g + 8) * kTld];
+          } else {       // A[l][m] = T[l][m]
+            a0 = Ts[(m0 + g) + (kk + t) * kTld];
+            a1 = Ts[(m0 + g + 8) + (kk + t) * kTld];
+          }
+          dmma(acc[u], a0, a1, W[(kk + t) + (n0 + g) * ldw]);
+        }
       }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int r = m0 + g + (e >> 1) * 8, c = n0 + 2 * t + (e & 1);
+      W2[r + c * ldw] = -(acc[0][e] + acc[1][e]);
     }
   }
   __syncthreads();
   prof_mark(PH_TRI);
-  // phase 3: Cv (nrows x wsz) += V W2; warp w owns m-tiles w, w+8 and all n-tiles
+  // phase 3: Cv (nrows x wsz) += V W2
   {
-    const int mt = (nrows + 15) >> 4, nt = (wsz + 7) >> 3;
-    double acc[2][8][4];
+    constexpr int MSTEP = kWarps / NT;              // m-tile stride of a warp
+    constexpr int MF = (kMaxNb / 16 + MSTEP - 1) / MSTEP;   // max fragments per warp
+    const int mt = (nrows + 15) >> 4;
+    const int n = warp % NT, mfirst = warp / NT;
+    if (n < nt) {
+      const int c0 = n * 8 + 2 * t;
+      double acc[MF][4];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int m0 = (warp + j * kWarps) * 16;
-#pragma unroll
-      for (int n = 0; n < 8; ++n)
+      for (int i = 0; i < MF; ++i) {
+        const int m0 = (mfirst + i * MSTEP) * 16;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int r = m0 + g + (e >> 1) * 8, c = n * 8 + 2 * t + (e & 1);
-          acc[j][n][e] = (m0 < nrows && n < nt) ? Cv[r + c * ldc] : 0.0;
-        }
-    }
-    for (int k = 0; k < kpad3; k += 4) {
-      double b[8];
-#pragma unroll
-      for (int n = 0; n < 8; ++n) b[n] = n < nt ? W2[(k + t) + (n * 8 + g) * ldw] : 0.0;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int m0 = (warp + j * kWarps) * 16;
-        if (warp + j * kWarps < mt) {
-          const double a0 = V[(m0 + g) + (k + t) * ldv];
-          const double a1 = V[(m0 + g + 8) + (k + t) * ldv];
-#pragma unroll
-          for (int n = 0; n < 8; ++n)
-            if (n < nt) dmma(acc[j][n], a0, a1, b[n]);
+          const int r = m0 + g + (e >> 1) * 8, c = c0 + (e & 1);
+          acc[i][e] = m0 < nrows ? Cv[r + c * ldc] : 0.0;
         }
       }
-    }
+      for (int k = 0; k < kpad3; k += 4) {
+        const double b = W2[(k + t) + (n * 8 + g) * ldw];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int m0 = (warp + j * kWarps) * 16;
-      if (m0 < nrows) {
+        for (int i = 0; i < MF; ++i) {
+          const int m = mfirst + i * MSTEP;
+          if (m < mt) {
+            const double a0 = V[(m * 16 + g) + (k + t) * ldv];
+            const double a1 = V[(m * 16 + g + 8) + (k + t) * ldv];
+            dmma(acc[i], a0, a1, b);
+          }
+        }
+      }
 #pragma unroll
-        for (int n = 0; n < 8; ++n)
+      for (int i = 0; i < MF; ++i) {
+        const int m0 = (mfirst + i * MSTEP) * 16;
+        if (m0 < nrows) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int r = m0 + g + (e >> 1) * 8, c = n * 8 + 2 * t + (e & 1);
-            if (n < nt && r < nrows && c < wsz) Cv[r + c * ldc] = acc[j][n][e];
+            const int r = m0 + g + (e >> 1) * 8, c = c0 + (e & 1);
+            if (r < nrows && c < wsz) Cv[r + c * ldc] = acc[i][e];
           }
+        }
       }
     }
   }
@@ -359,6 +382,13 @@ __device__ void apply_block(double *Ctop, double *Cv, int ldc, int nrows, const 
   }
   __syncthreads();
   prof_mark(PH_MMA3);
+}
+
+__device__ __forceinline__ void apply_block(double *Ctop, double *Cv, int ldc, int nrows, const double *V,
+                                            int ldv, const double *Ts, int bw, int wsz, bool trans, double *W,
+                                            double *W2) {
+  if (wsz <= 32) apply_block_t<4>(Ctop, Cv, ldc, nrows, V, ldv, Ts, bw, wsz, trans, W, W2);
+  else apply_block_t<8>(Ctop, Cv, ldc, nrows, V, ldv, Ts, bw, wsz, trans, W, W2);
 }
 
 // ---- warp reduce-scatter: lane l ends with sum over lanes of v[l] (v[0]) ----
@@ -624,7 +654,7 @@ __device__ void panel_block(double *X, double *A1, double *Tslot, int nb, int ib
 template <int MODE>
 __device__ void panel_task(double *X, double *A1, double *Tslot, int nb, int ib, int ws, double *smem,
                            const SmemLayout &L) {
-  double *Cb = smem + L.offC, *Vb = smem + L.offV, *Wb = smem + L.offW, *Ts = smem + L.offT;
+  double *Cb = smem + L.offC, *Vb = smem + L.offV[0], *Wb = smem + L.offW, *Ts = smem + L.offT[0];
   for (int j0 = 0; j0 < nb; j0 += ib) {
     const int bw = min(ib, nb - j0);
     panel_block<MODE>(X, A1, Tslot, nb, ib, j0, bw, Vb, L.ldv, Ts, Wb);
@@ -641,14 +671,14 @@ __device__ void panel_task(double *X, double *A1, double *Tslot, int nb, int ib,
         store_rows(Cb, L.ldc, 0, X, nb, j0, nb, cs, wsz);
       } else {
         const int r2 = MODE == 1 ? j0 + bw : nb;
-        load_rows(Cb, L.ldc, 0, A1, nb, j0, j0 + bw, cs, wsz);
-        load_rows(Cb, L.ldc, nb, X, nb, 0, r2, cs, wsz);
+        async_block(Cb, L.ldc, A1, nb, j0, j0 + bw, cs, wsz);         // C1 rows of the block -> window 0
+        load_rows(Cb, L.ldc, kWinRows, X, nb, 0, r2, cs, wsz);
         cp_async_wait_all();
         __syncthreads();
         prof_mark(PH_LOAD);
-        apply_block(Cb + j0, Cb + nb, L.ldc, r2, Vb, L.ldv, Ts, bw, wsz, true, Wb, Wb + L.ldw * L.wcols);
-        store_rows(Cb, L.ldc, 0, A1, nb, j0, j0 + bw, cs, wsz);
-        store_rows(Cb, L.ldc, nb, X, nb, 0, r2, cs, wsz);
+        apply_block(Cb, Cb + kWinRows, L.ldc, r2, Vb, L.ldv, Ts, bw, wsz, true, Wb, Wb + L.ldw * L.wcols);
+        store_rows(Cb - j0, L.ldc, 0, A1, nb, j0, j0 + bw, cs, wsz);
+        store_rows(Cb, L.ldc, kWinRows, X, nb, 0, r2, cs, wsz);
       }
     }
     __syncthreads();
@@ -656,60 +686,107 @@ __device__ void panel_task(double *X, double *A1, double *Tslot, int nb, int ib,
 }
 
 // ---- update kernels on one column strip -----------------------------------
+// Inner blocks are pipelined: while block b is applied, the V / T (and C1
+// rows) of the next block stream into the other buffer (when smem allows).
+
 // UNMQR: C (tile strip) <- Q^T C (or Q C) with inner blocks [b_lo, b_hi) of the
 // GEQRT reflectors of tile Vt; only rows >= b_lo*ib are touched.
 __device__ void unmqr_strip(const double *Vt, const double *Tslot, double *Ct, int nb, int ib, int cs,
-                            int wsz, bool trans, int b_lo, int b_hi, double *smem, const SmemLayout &L) {
-  double *Cb = smem + L.offC, *Vb = smem + L.offV, *Wb = smem + L.offW, *Ts = smem + L.offT;
+                            int wsz, bool trans, int b_lo, int b_hi, double *smem, const SmemLayout &L,
+                            bool resident = false) {
+  double *Cb = smem + L.offC, *Wb = smem + L.offW;
   const int r0 = b_lo * ib;
+  const int nblk = b_hi - b_lo;
+  auto blk = [&](int idx) { return trans ? b_lo + idx : b_hi - 1 - idx; };
   load_rows(Cb, L.ldc, 0, Ct, nb, r0, nb, cs, wsz);
-  for (int t = b_lo; t < b_hi; ++t) {
-    const int b = trans ? t : b_hi - 1 - (t - b_lo);
-    const int j0 = b * ib, bw = min(ib, nb - j0);
-    issue_v_geqrt(Vb, L.ldv, Vt, nb, j0, bw);
-    issue_t(Ts, Tslot, ib, j0, bw);
+  if (!resident) {     // resident: the panel task just left V (unit diagonal, padded) and T in buffer 0
+    const int j0 = blk(0) * ib, bw = min(ib, nb - j0);
+    issue_v_geqrt(smem + L.offV[0], L.ldv, Vt, nb, j0, bw);
+    issue_t(smem + L.offT[0], Tslot, ib, j0, bw);
+  }
+  for (int idx = 0; idx < nblk; ++idx) {
+    const int cur = idx & (L.nvb - 1);
+    double *Vb = smem + (cur ? L.offV[1] : L.offV[0]), *Ts = smem + (cur ? L.offT[1] : L.offT[0]);
+    const int j0 = blk(idx) * ib, bw = min(ib, nb - j0);
     cp_async_wait_all();
     __syncthreads();
     prof_mark(PH_LOAD);
-    fix_v_geqrt(Vb, L.ldv, nb, j0, bw);
-    __syncthreads();
+    if (!(resident && idx == 0)) {
+      fix_v_geqrt(Vb, L.ldv, nb, j0, bw);
+      __syncthreads();
+    }
     prof_mark(PH_FIX);
+    if (L.nvb == 2 && idx + 1 < nblk) {
+      const int j1 = blk(idx + 1) * ib, bw1 = min(ib, nb - j1);
+      issue_v_geqrt(smem + (cur ? L.offV[0] : L.offV[1]), L.ldv, Vt, nb, j1, bw1);
+      issue_t(smem + (cur ? L.offT[0] : L.offT[1]), Tslot, ib, j1, bw1);
+    }
     apply_block(nullptr, Cb + j0, L.ldc, nb - j0, Vb, L.ldv, Ts, bw, wsz, trans, Wb, Wb + L.ldw * L.wcols);
+    if (L.nvb == 1 && idx + 1 < nblk) {
+      const int j1 = blk(idx + 1) * ib, bw1 = min(ib, nb - j1);
+      issue_v_geqrt(Vb, L.ldv, Vt, nb, j1, bw1);
+      issue_t(Ts, Tslot, ib, j1, bw1);
+    }
   }
   store_rows(Cb, L.ldc, 0, Ct, nb, r0, nb, cs, wsz);
 }
 
 // TTMQR / TSMQR: [C1; C2] <- Q^T [C1; C2] (or Q) with inner blocks [b_lo, b_hi)
 // of the TTQRT/TSQRT reflectors V2 of tile Vt. Block b touches C1 rows
-// b*ib .. b*ib+bw-1 and C2 rows 0 .. (tri ? b*ib+bw : nb)-1.
+// b*ib .. b*ib+bw-1 (streamed through a 32-row window) and C2 rows
+// 0 .. (tri ? b*ib+bw : nb)-1 (resident).
 __device__ void tpmqr_strip(const double *Vt, const double *Tslot, double *C1, double *C2, int nb, int ib,
                             int cs, int wsz, bool tri, bool trans, int b_lo, int b_hi, double *smem,
-                            const SmemLayout &L) {
-  double *Cb = smem + L.offC, *Vb = smem + L.offV, *Wb = smem + L.offW, *Ts = smem + L.offT;
-  const int r1lo = b_lo * ib, r1hi = min(b_hi * ib, nb), r2hi = tri ? r1hi : nb;
-  load_rows(Cb, L.ldc, 0, C1, nb, r1lo, r1hi, cs, wsz);
-  load_rows(Cb, L.ldc, nb, C2, nb, 0, r2hi, cs, wsz);
-  for (int t = b_lo; t < b_hi; ++t) {
-    const int b = trans ? t : b_hi - 1 - (t - b_lo);
-    const int j0 = b * ib, bw = min(ib, nb - j0);
-    issue_v_tp(Vb, L.ldv, Vt, nb, j0, bw, tri);
-    issue_t(Ts, Tslot, ib, j0, bw);
+                            const SmemLayout &L, bool resident = false) {
+  double *Cb = smem + L.offC, *Wb = smem + L.offW;
+  const int r2hi = tri ? min(b_hi * ib, nb) : nb;
+  const int nblk = b_hi - b_lo;
+  auto blk = [&](int idx) { return trans ? b_lo + idx : b_hi - 1 - idx; };
+  load_rows(Cb, L.ldc, kWinRows, C2, nb, 0, r2hi, cs, wsz);
+  {
+    const int j0 = blk(0) * ib, bw = min(ib, nb - j0);
+    if (!resident) {
+      issue_v_tp(smem + L.offV[0], L.ldv, Vt, nb, j0, bw, tri);
+      issue_t(smem + L.offT[0], Tslot, ib, j0, bw);
+    }
+    async_block(Cb, L.ldc, C1, nb, j0, j0 + bw, cs, wsz);
+  }
+  for (int idx = 0; idx < nblk; ++idx) {
+    const int cur = idx & (L.nvb - 1);
+    double *Vb = smem + (cur ? L.offV[1] : L.offV[0]), *Ts = smem + (cur ? L.offT[1] : L.offT[0]), *win = Cb + 32 * (idx & 1);
+    const int j0 = blk(idx) * ib, bw = min(ib, nb - j0);
     cp_async_wait_all();
     __syncthreads();
     prof_mark(PH_LOAD);
-    fix_v_tp(Vb, L.ldv, nb, j0, bw, tri);
-    __syncthreads();
+    if (!(resident && idx == 0)) {
+      fix_v_tp(Vb, L.ldv, nb, j0, bw, tri);
+      __syncthreads();
+    }
     prof_mark(PH_FIX);
-    apply_block(Cb + j0, Cb + nb, L.ldc, tri ? j0 + bw : nb, Vb, L.ldv, Ts, bw, wsz, trans, Wb, Wb + L.ldw * L.wcols);
+    if (L.nvb == 2 && idx + 1 < nblk) {
+      const int j1 = blk(idx + 1) * ib, bw1 = min(ib, nb - j1);
+      issue_v_tp(smem + (cur ? L.offV[0] : L.offV[1]), L.ldv, Vt, nb, j1, bw1, tri);
+      issue_t(smem + (cur ? L.offT[0] : L.offT[1]), Tslot, ib, j1, bw1);
+      async_block(Cb + 32 * ((idx + 1) & 1), L.ldc, C1, nb, j1, j1 + bw1, cs, wsz);
+    }
+    apply_block(win, Cb + kWinRows, L.ldc, tri ? j0 + bw : nb, Vb, L.ldv, Ts, bw, wsz, trans, Wb,
+                Wb + L.ldw * L.wcols);
+    store_rows(win - j0, L.ldc, 0, C1, nb, j0, j0 + bw, cs, wsz);
+    if (L.nvb == 1 && idx + 1 < nblk) {
+      __syncthreads();
+      const int j1 = blk(idx + 1) * ib, bw1 = min(ib, nb - j1);
+      issue_v_tp(Vb, L.ldv, Vt, nb, j1, bw1, tri);
+      issue_t(Ts, Tslot, ib, j1, bw1);
+      async_block(Cb + 32 * ((idx + 1) & 1), L.ldc, C1, nb, j1, j1 + bw1, cs, wsz);
+    }
   }
-  store_rows(Cb, L.ldc, 0, C1, nb, r1lo, r1hi, cs, wsz);
-  store_rows(Cb, L.ldc, nb, C2, nb, 0, r2hi, cs, wsz);
+  store_rows(Cb, L.ldc, kWinRows, C2, nb, 0, r2hi, cs, wsz);
 }
 
-__device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const SmemLayout &L) {
+__device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const SmemLayout &L, bool resident) {
   const int p = a.p, nb = a.nb, ib = a.ib, ws = a.ws;
   const int nblk = (nb + ib - 1) / ib;
-  double *Vb = smem + L.offV, *Wb = smem + L.offW, *Ts = smem + L.offT;
+  double *Vb = smem + L.offV[0], *Wb = smem + L.offW, *Ts = smem + L.offT[0];
   switch (t.kind) {
     case K_GEQRT:
       panel_task<0>(tile_ptr(a.A, p, nb, t.i, t.k), nullptr, tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0), nb, ib, ws,
@@ -742,7 +819,8 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
     case K_GEQRT_U: {
       const int cs = t.s * ws, wsz = min(ws, nb - cs);
       double *X = tile_ptr(a.A, p, nb, t.i, t.k);
-      unmqr_strip(X, tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0), X, nb, ib, cs, wsz, true, t.j, t.j + 1, smem, L);
+      unmqr_strip(X, tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0), X, nb, ib, cs, wsz, true, t.j, t.j + 1, smem, L,
+                  resident);
       break;
     }
     case K_TTQRT_U:
@@ -750,7 +828,7 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
       const int cs = t.s * ws, wsz = min(ws, nb - cs);
       double *X = tile_ptr(a.A, p, nb, t.i, t.k);
       tpmqr_strip(X, tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1), tile_ptr(a.A, p, nb, t.piv, t.k), X, nb, ib, cs, wsz,
-                  t.kind == K_TTQRT_U, true, t.j, t.j + 1, smem, L);
+                  t.kind == K_TTQRT_U, true, t.j, t.j + 1, smem, L, resident);
       break;
     }
     // ---- updates of other tiles (factorization) and of C (apply)
@@ -808,7 +886,7 @@ __device__ __forceinline__ void st_release64(unsigned long long *p, unsigned lon
   asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __forceinline__ void push_ready(const RunArgs &a, int t) {
+__device__ __forceinline__ void push_ready(const RunArgs &a, int t) {   // (chained tasks may be queued too)
   const int q = (a.tasks[t].meta >> 16) & 1 ? 0 : 1;     // 0 = panel chain queue
   const int pos = atomicAdd(&a.ctrl[kCtrlTail + 8 * q], 1);
   st_release64(a.queue + (size_t)q * a.ntask + pos, ((unsigned long long)(unsigned)a.epoch << 32) | (unsigned)t);
@@ -832,11 +910,24 @@ __device__ __forceinline__ int try_pop(const RunArgs &a, int q) {
   return -1;
 }
 
+__device__ __forceinline__ unsigned ld_acquire_u(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned need_count(const RunArgs &a, int t) {
+  const int m = a.tasks[t].meta;
+  return (unsigned)a.epoch * (unsigned)((m & 0xffff) + ((m >> 17) & 1));
+}
+__device__ __forceinline__ bool is_panel_block(int kind) {
+  return kind == K_GEQRT_B || kind == K_TTQRT_B || kind == K_TSQRT_B;
+}
+
 __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ int s_task;
+  __shared__ int s_task, s_chain, s_resident;
   const SmemLayout L = smem_layout(a.nb, a.ib, a.ws);
-  if (threadIdx.x == 0) s_prof_on = 0;
+  if (threadIdx.x == 0) { s_prof_on = 0; s_chain = -1; s_resident = 0; }
   // everything the DMMA padding may read must be finite: start from zeros
   for (size_t x = threadIdx.x; x < L.total; x += kThreads) smem[x] = 0.0;
   if (threadIdx.x == 0)
@@ -844,14 +935,17 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
   for (;;) {
     if (threadIdx.x == 0) {
       unsigned long long t_take = a.trace ? globaltimer() : 0ull;
-      int t;
-      for (;;) {
-        if (ld_relaxed(&a.ctrl[kCtrlDone]) >= a.ntask) { t = -1; break; }
-        t = try_pop(a, 0);
-        if (t >= 0) break;
-        t = try_pop(a, 1);
-        if (t >= 0) break;
-        __nanosleep(64);
+      int t = s_chain;
+      if (t < 0) {
+        s_resident = 0;
+        for (;;) {
+          if (ld_relaxed(&a.ctrl[kCtrlDone]) >= a.ntask) { t = -1; break; }
+          t = try_pop(a, 0);
+          if (t >= 0) break;
+          t = try_pop(a, 1);
+          if (t >= 0) break;
+          __nanosleep(64);
+        }
       }
       s_task = t;
       if (a.trace && t >= 0) {
@@ -867,15 +961,14 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
     if (t < 0) break;
     __threadfence();
     const DevTask tk = a.tasks[t];
-    run_task(a, tk, smem, L);
+    run_task(a, tk, smem, L, s_resident != 0);
     __syncthreads();
     prof_mark(PH_STORE);
     if (threadIdx.x == 0) {
       __threadfence();
       for (int x = tk.dep_begin; x < tk.dep_end; ++x) {
         const int sc = a.succ[x];
-        const unsigned need = (unsigned)a.epoch * (unsigned)(a.tasks[sc].meta & 0xffff);
-        if (atom_add_acqrel(a.cnt + sc, 1u) + 1u == need) push_ready(a, sc);
+        if (atom_add_acqrel(a.cnt + sc, 1u) + 1u == need_count(a, sc)) push_ready(a, sc);
       }
       if (a.trace) {
         unsigned long long *tr = a.trace + kTraceWords * (size_t)t;
@@ -884,6 +977,18 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
         for (int x = 0; x < 8; ++x) tr[4 + x] = s_prof[x];
       }
       atomicAdd(&a.ctrl[kCtrlDone], 1);
+      // panel chain: run the chained successor here if its other inputs are (or
+      // soon become) ready; otherwise release the virtual dependency so the last
+      // real predecessor queues it normally. Either way it runs exactly once.
+      int nxt = -1;
+      if (tk.chain >= 0) {
+        const int c = tk.chain;
+        const unsigned need = need_count(a, c);
+        for (int it = 0; it < 64 && ld_acquire_u(a.cnt + c) + 1u < need; ++it) __nanosleep(128);
+        if (atom_add_acqrel(a.cnt + c, 1u) + 1u == need) nxt = c;
+      }
+      s_resident = (nxt >= 0 && is_panel_block(tk.kind)) ? 1 : 0;
+      s_chain = nxt;
     }
   }
   if (threadIdx.x == 0) {

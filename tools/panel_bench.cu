@@ -15,9 +15,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_panel(double *X, double *T, int
   long long t0 = clock64();
   if (threadIdx.x == 0) s_prof_last = t0;
   if (mode == 0)
-    panel_block<0>(X, nullptr, T, nb, ib, 0, 32, smem + L.offV, L.ldv, smem + L.offT, smem + L.offW);
+    panel_block<0>(X, nullptr, T, nb, ib, 0, 32, smem + L.offV[0], L.ldv, smem + L.offT[0], smem + L.offW);
   else
-    panel_block<1>(X, X + nb * nb, T, nb, ib, nb - 32, 32, smem + L.offV, L.ldv, smem + L.offT, smem + L.offW);
+    panel_block<1>(X, X + nb * nb, T, nb, ib, nb - 32, 32, smem + L.offV[0], L.ldv, smem + L.offT[0], smem + L.offW);
   __syncthreads();
   long long t1 = clock64();
   if (threadIdx.x == 0) { out[0] = t1 - t0; for (int i = 0; i < 8; ++i) out[1 + i] = s_prof[i]; }
