@@ -51,8 +51,14 @@ enum tqr_tree {
   TQR_FIBONACCI = 1,  /* Fibonacci scheme of order 1, lines 490-505 */
   TQR_GREEDY = 2,     /* Greedy, lines 507-512 and Algorithm 4 (lines 563-619) */
   TQR_BINARY = 3,     /* BinaryTree, lines 914-918 */
-  TQR_PLASMA = 4      /* PlasmaTree(BS): flat inside domains of BS rows + binary
+  TQR_PLASMA = 4,     /* PlasmaTree(BS): flat inside domains of BS rows + binary
                          merge of the domain heads, lines 936-953 */
+  TQR_MERGE = 5       /* merge of two stacked tile-upper-triangular R factors
+                         [R1; R2] (p = 2q): column k zeroes tiles (q+t, k),
+                         t = 1..k, against pivot row k. Used by the cross-GPU
+                         reduction of tall-skinny matrices: the
+                         input's diagonal tiles count as triangles, tiles below
+                         them as structural zeros (they must hold zeros). */
 };
 
 /* Kernel families, §2.1 (lines 231-352) */

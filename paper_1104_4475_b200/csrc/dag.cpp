@@ -20,13 +20,16 @@
 
 namespace tqr {
 
-void expand(const std::vector<Elim> &lst, int p, int q, int family, std::vector<TileTask> &tasks) {
+void expand(const std::vector<Elim> &lst, int p, int q, int family, std::vector<TileTask> &tasks,
+            bool merge_input) {
   tasks.clear();
   const int kmax = std::min(p, q);
   std::vector<int> last((size_t)(p + 1) * (q + 1), -1);   // last writer per tile (1-based)
   std::vector<char> tri((size_t)(p + 1) * (q + 1), 0);
   std::vector<int> geqrt_of((size_t)(p + 1) * (q + 1), -1);
   auto at = [q](int r, int c) { return (size_t)r * (q + 1) + c; };
+  if (merge_input)    // [R1; R2]: both diagonals of tiles are already triangles
+    for (int k = 1; k <= q; ++k) tri[at(k, k)] = tri[at(q + k, k)] = 1;
 
   auto emit = [&](int kind, int i, int piv, int k, int j, int reads, std::initializer_list<std::pair<int, int>> writes) {
     TileTask t{kind, i, piv, k, j, {}};

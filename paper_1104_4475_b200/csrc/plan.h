@@ -32,7 +32,10 @@ struct TileTask {
 };
 
 // Expansion of an elimination list into kernel tasks (dag.cpp), in emission order.
-void expand(const std::vector<Elim> &lst, int p, int q, int family, std::vector<TileTask> &tasks);
+// merge_input: the matrix is [R1; R2] (p = 2q) whose diagonal tiles are
+// already triangles and whose lower tiles are structurally zero.
+void expand(const std::vector<Elim> &lst, int p, int q, int family, std::vector<TileTask> &tasks,
+            bool merge_input = false);
 
 // Discrete-event simulation with unbounded processors; returns makespan.
 int64_t simulate(const std::vector<TileTask> &tasks, std::vector<int64_t> &start,

@@ -60,7 +60,7 @@ static int tile_sim(int p, int q, int tree, int bs, int family, std::vector<Tile
   std::string err;
   if (family != TQR_TT && family != TQR_TS) return fail(TQR_EINVAL, "unknown kernel family");
   if (!build_elim_list(p, q, tree, bs, lst, err)) return fail(TQR_EINVAL, err);
-  expand(lst, p, q, family, tt);
+  expand(lst, p, q, family, tt, tree == TQR_MERGE);
   mk = simulate(tt, st, fin);
   return 0;
 }

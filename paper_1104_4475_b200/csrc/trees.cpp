@@ -121,6 +121,16 @@ void coarse_asap(int p, std::vector<Elim> &lst) {
   }
 }
 
+// ---- Merge of two stacked tile-upper-triangular R factors [R1; R2] (2q x q
+// tiles): column k zeroes the bottom tiles (q+t, k), t = 1..k,
+// against the top pivot row k (flat within the merge). Bottom row q+t has
+// structural zeros left of column t, so it is ready for column k once it was
+// eliminated in columns t..k-1 (validity conditions, lines 362-369).
+void merge(int q, std::vector<Elim> &out) {
+  for (int k = 1; k <= q; ++k)
+    for (int t = 1; t <= k; ++t) out.push_back({q + t, k, k, 0});
+}
+
 }  // namespace
 
 bool build_elim_list(int p, int q, int tree, int bs, std::vector<Elim> &out, std::string &err) {
@@ -134,6 +144,9 @@ bool build_elim_list(int p, int q, int tree, int bs, std::vector<Elim> &out, std
     case 4:
       if (bs < 1 || bs > p) { err = "elim_list: PlasmaTree needs 1 <= bs <= p"; return false; }
       plasma(p, q, bs, out); coarse_asap(p, out); break;
+    case 5:
+      if (p != 2 * q) { err = "elim_list: the merge scheme needs p = 2q"; return false; }
+      merge(q, out); coarse_asap(p, out); break;
     default: err = "elim_list: unknown tree"; return false;
   }
   if (tree == 1 || tree == 2) {

@@ -174,3 +174,48 @@ def test_config1_full_size_properties(tree, bs):
     Q = gpu_Q(buf, T, m, n, nb, ib, tree, bs, "TT")
     assert np.linalg.norm(A - Q @ R) / np.linalg.norm(A) <= TOL_QR
     assert np.linalg.norm(np.eye(n) - Q.T @ Q) <= TOL_QR
+
+
+@pytest.mark.parametrize("q,nb,ib,family", [(3, 64, 32, "TT"), (2, 24, 8, "TT"), (3, 40, 32, "TS")])
+def test_merge_kernel(q, nb, ib, family):
+    """TT merge of two stacked tile-triangular R factors (tree "merge", used by the
+    cross-GPU reduction): R equals LAPACK's R of [R1; R2] up to row signs, and
+    the stored Q reproduces the input (apply_q on the device)."""
+    n = q * nb
+    R1 = np.triu(qrinputs.gaussian(n, n, 5))
+    R2 = np.triu(qrinputs.gaussian(n, n, 6))
+    S = np.asfortranarray(np.vstack([R1, R2]))
+    buf, T = run_gpu(S, nb, ib, "merge", 1, family)
+    got = qrinputs.from_tiles(buf.cpu().numpy(), 2 * q, q, nb)
+    R = np.triu(got[:n])
+    Rl = np.linalg.qr(S, mode="r")
+    assert rel(nu.sign_normalise(R), nu.sign_normalise(Rl)) <= TOL_R
+    Q = gpu_Q(buf, T, 2 * n, n, nb, ib, "merge", 1, family)
+    assert np.linalg.norm(S - Q @ R) / np.linalg.norm(S) <= TOL_QR
+    assert np.linalg.norm(np.eye(n) - Q.T @ Q) <= TOL_QR
+
+
+@pytest.mark.parametrize("world,tree", [(4, "greedy"), (3, "fibonacci"), (2, "flat")])
+def test_tall_skinny_domains_on_one_gpu(world, tree):
+    """The configs[3] algorithm with `world` domains executed one after another on
+    one GPU (independent launches, no inter-kernel waiting): local tiled QR per
+    domain, then the binary merge tree of paper_1104_4475_b200.dist; the final R
+    equals LAPACK's R of the whole matrix."""
+    from paper_1104_4475_b200 import dist as tdist
+    p, q, nb, ib = 9, 2, 64, 32
+    A = qrinputs.gaussian(p * nb, q * nb, 99)
+    Rs = []
+    for r in range(world):
+        r0, r1 = tdist.domain(p, world, r)
+        loc = torch.from_numpy(qrinputs.to_tiles(np.asfortranarray(A[r0 * nb:r1 * nb]), nb)).to(DEV)
+        tq.tiled_qr(loc, (r1 - r0) * nb, q * nb, nb, ib, tree, 1, "TT")
+        Rs.append(tdist.extract_r(loc, r1 - r0, q, nb))
+    for pairs in tdist.merge_schedule(world):
+        for dst, src in pairs:
+            M = tdist.stack_pair(Rs[dst], Rs[src], q, nb)
+            tq.tiled_qr(M, 2 * q * nb, q * nb, nb, ib, "merge", 1, "TT")
+            Rs[dst] = tdist.top_r(M, q, nb)
+    torch.cuda.synchronize()
+    R = np.triu(qrinputs.from_tiles(Rs[0].cpu().numpy(), q, q, nb))
+    Rl = np.linalg.qr(A, mode="r")
+    assert rel(nu.sign_normalise(R), nu.sign_normalise(Rl)) <= TOL_R
