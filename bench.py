@@ -276,6 +276,85 @@ def run_gpu(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# configs[3]: tall-skinny, tile rows split across ranks, binary TT merge over NCCL
+# ---------------------------------------------------------------------------
+TALL = dict(p=2048, q=16, nb=256, ib=32)
+
+
+def run_tall(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_1104_4475_b200 as tq
+    from paper_1104_4475_b200 import dist as tdist
+
+    p = args.tall_p or TALL["p"]
+    q, nb, ib = TALL["q"], TALL["nb"], TALL["ib"]
+    tree = args.tree
+    m, n = p * nb, q * nb
+    flops = 2.0 * n * n * (m - n / 3.0)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    r0, r1 = tdist.domain(p, world, rank)
+    p_loc = r1 - r0
+    g = torch.Generator(device=dev).manual_seed(SEED + 7919 * rank)
+    A0 = torch.randn(p_loc * q * nb * nb, dtype=torch.float64, device=dev, generator=g)   # i.i.d. N(0,1)
+    A = torch.empty_like(A0)
+    stream = torch.cuda.current_stream()
+
+    def one(times):
+        A.copy_(A0)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        tdist.tall_skinny_qr(A, p, q, nb, ib, tree, 1, "TT")
+        e1.record(stream)
+        times.append((e0, e1))
+
+    for _ in range(args.warmup):
+        one([])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = []
+    with Clocks(local_rank) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for _ in range(args.steps):
+            one(ev)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = sum(e0.elapsed_time(e1) for e0, e1 in ev)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    value = flops * args.steps / (max_ms / 1e3) / 1e9
+    if rank != 0:
+        return
+    peak, peak_src = fp64_peak()
+    print(json.dumps({
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"configs[3]: tall-skinny fp64 tiled QR {m}x{n} (p={p} x q={q} tiles, nb={nb}, "
+                               f"ib={ib}), i.i.d. N(0,1), tile-row domains per GPU reduced locally by {tree}, "
+                               f"then a binary TT merge of the q x q R factors across GPUs (NCCL send/recv)",
+                   "parallelism": f"tile-row domains x{world}",
+                   "l2": "inputs (17 GB at full size) far exceed L2; restored by a device copy outside the events",
+                   "timing": "CUDA events around tall_skinny_qr per rank (local factor + merges + NCCL), max over ranks"},
+        "fp64_peak_frac": value / 1e3 / (peak * world),
+        "roofline": {"bound": "tensor", "achieved": value / 1e3 / world, "peak": peak, "unit": "TFLOP/s",
+                     "frac": value / 1e3 / world / peak, "traffic": None, "kernel": "tqr_persistent",
+                     "peak_source": peak_src},
+        "clocks": clk.summary(),
+        "e2e": None,
+        "gpu_launches": (1 + len(tdist.merge_schedule(world))) * args.steps,
+    }), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -283,6 +362,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="square", choices=["square", "tall"],
+                    help="square = configs[1] (default); tall = configs[3] partitioned over the ranks")
+    ap.add_argument("--tree", default="greedy", help="tree of the local factorizations (tall workload)")
+    ap.add_argument("--tall-p", type=int, default=0, help="override p of the tall workload (testing)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -296,7 +379,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_gpu(args, rank, world, local_rank)
+        if args.workload == "tall":
+            run_tall(args, rank, world, local_rank)
+        else:
+            run_gpu(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist
