@@ -278,7 +278,7 @@ void build_apply_graph(const std::vector<TileTask> &tt, int p, int qc, int nb, i
   reorder(g, key, deps);
 }
 
-void finalize_dataflow(DevGraph &g) {
+void finalize_dataflow(DevGraph &g, bool lookahead) {
   const int n = (int)g.tasks.size();
   std::vector<int32_t> cnt(n + 1, 0);
   for (int t = 0; t < n; ++t)
@@ -297,9 +297,13 @@ void finalize_dataflow(DevGraph &g) {
   for (int t = 0; t < n; ++t) {
     DevTask &x = g.tasks[t];
     const int indeg = x.dep_end - x.dep_begin;
+    // panel chain + look-ahead: the panels, the update of the next strip inside a
+    // split panel, and the updates of the next panel column (j = k+1)
+    const bool upd = x.kind == K_UNMQR || x.kind == K_TTMQR || x.kind == K_TSMQR;
     const bool hi = x.kind == K_GEQRT || x.kind == K_TTQRT || x.kind == K_TSQRT || x.kind == K_GEQRT_B ||
                     x.kind == K_TTQRT_B || x.kind == K_TSQRT_B ||
-                    ((x.kind == K_GEQRT_U || x.kind == K_TTQRT_U || x.kind == K_TSQRT_U) && x.s == x.j + 1);
+                    ((x.kind == K_GEQRT_U || x.kind == K_TTQRT_U || x.kind == K_TSQRT_U) && x.s == x.j + 1) ||
+                    (lookahead && upd && x.j == x.k + 1);
     x.meta = indeg | ((hi ? 1 : 0) << 16) | (chained[t] ? 1 << 17 : 0);
     x.dep_begin = cnt[t];
     x.dep_end = cnt[t + 1];

@@ -67,7 +67,7 @@ struct DevGraph {
 // priority class of every task (1 = panel chain: panel kernels and the
 // look-ahead strip update of split panels; 0 = other updates); chain targets
 // get meta bit 17 (one virtual extra dependency held by the chain owner).
-void finalize_dataflow(DevGraph &g);
+void finalize_dataflow(DevGraph &g, bool lookahead = true);
 
 // Strip-refined factorization graph: every update task is split into
 // ceil(nb/ws) column strips of width ws; with split_panels (requires ws == ib)

@@ -155,7 +155,8 @@ static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, in
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   int ws = pick_ws(nb, ib);
-  PlanKey key{dev, mode, p, q, qc, nb, ib, tree, bs, family, ws * 2 + (env_int("TQR_SPLIT", 1) != 0)};
+  PlanKey key{dev, mode, p, q, qc, nb, ib, tree, bs, family,
+              ws * 4 + (env_int("TQR_SPLIT", 1) != 0) * 2 + (env_int("TQR_LOOKAHEAD", 1) != 0)};
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_plans.find(key);
   if (it != g_plans.end()) { *out = it->second.get(); return 0; }
@@ -168,7 +169,7 @@ static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, in
   const bool split = env_int("TQR_SPLIT", 1) != 0 && ws == ib && nb > ib;
   if (mode == 0) build_factor_graph(tt, st, p, q, nb, ws, split, g);
   else build_apply_graph(tt, p, qc, nb, ws, mode == 1, g);
-  finalize_dataflow(g);
+  finalize_dataflow(g, env_int("TQR_LOOKAHEAD", 1) != 0);
   auto pl = std::make_unique<DevPlan>();
   rc = upload(g, ws, *pl);
   if (rc < 0) return rc;

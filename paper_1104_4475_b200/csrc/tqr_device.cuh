@@ -199,7 +199,7 @@ __device__ __forceinline__ void issue_v_geqrt(double *V, int ldv, const double *
   async_block(V, ldv, X, nb, j0, nb, j0, bw);
 }
 __device__ __forceinline__ void fix_v_geqrt(double *V, int ldv, int nb, int j0, int bw) {
-  const int nr = nb - j0, nr4 = (nr + 3) & ~3;
+  const int nr = nb - j0, nr4 = (nr + 15) & ~15;
   for (int idx = threadIdx.x; idx < bw * bw; idx += kThreads) {
     const int rr = idx % bw, l = idx / bw;
     if (rr <= l && rr < nr) V[rr + l * ldv] = rr == l ? 1.0 : 0.0;
@@ -213,7 +213,7 @@ __device__ __forceinline__ void issue_v_tp(double *V, int ldv, const double *X, 
   async_block(V, ldv, X, nb, 0, tri ? j0 + bw : nb, j0, bw);
 }
 __device__ __forceinline__ void fix_v_tp(double *V, int ldv, int nb, int j0, int bw, bool tri) {
-  const int nr = tri ? j0 + bw : nb, nr4 = (nr + 3) & ~3;
+  const int nr = tri ? j0 + bw : nb, nr4 = (nr + 15) & ~15;
   if (tri) {
     for (int idx = threadIdx.x; idx < bw * bw; idx += kThreads) {
       const int rr = idx % bw, l = idx / bw;
@@ -223,9 +223,9 @@ __device__ __forceinline__ void fix_v_tp(double *V, int ldv, int nb, int j0, int
   const int pad = nr4 - nr;
   for (int idx = threadIdx.x; idx < pad * bw; idx += kThreads) V[nr + idx % pad + (idx / pad) * ldv] = 0.0;
 }
-// zero V rows [nr, round_up(nr, 4)) of columns 0..bw-1
+// zero V rows [nr, round_up(nr, 16)) of columns 0..bw-1 (K padding of the DMMA loops)
 __device__ __forceinline__ void zero_vpad(double *V, int ldv, int nr, int bw) {
-  const int pad = ((nr + 3) & ~3) - nr;
+  const int pad = ((nr + 15) & ~15) - nr;
   for (int idx = threadIdx.x; idx < pad * bw; idx += kThreads) V[nr + idx % pad + (idx / pad) * ldv] = 0.0;
 }
 // T block (bw x bw upper triangular) of columns j0.. of a T slot -> Ts (ld kTld);
@@ -259,6 +259,39 @@ __device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, doubl
 // chains per warp: K is interleaved over 4 chains in phase 1 and 2 chains in
 // phase 2, and phase 3 deals the (m16, n8) fragments round-robin over warps
 // (warp w: n-tile w mod NT, m-tiles w / NT + i * 8 / NT).
+// Cv += V W2 for NF fragments (m-tiles mfirst, mfirst+MSTEP, ...) of n-tile n
+template <int NF, int MSTEP>
+__device__ __forceinline__ void phase3_frags(double *Cv, int ldc, int nrows, const double *V, int ldv,
+                                             const double *W2, int wsz, int n, int mfirst, int kpad3) {
+  constexpr int ldw = 36;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int c0 = n * 8 + 2 * t;
+  double acc[NF][4];
+#pragma unroll
+  for (int i = 0; i < NF; ++i) {
+    const int m0 = (mfirst + i * MSTEP) * 16;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[i][e] = Cv[(m0 + g + (e >> 1) * 8) + (c0 + (e & 1)) * ldc];
+  }
+  for (int k = 0; k < kpad3; k += 4) {
+    const double b = W2[(k + t) + (n * 8 + g) * ldw];
+#pragma unroll
+    for (int i = 0; i < NF; ++i) {
+      const int m0 = (mfirst + i * MSTEP) * 16;
+      dmma(acc[i], V[(m0 + g) + (k + t) * ldv], V[(m0 + g + 8) + (k + t) * ldv], b);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NF; ++i) {
+    const int m0 = (mfirst + i * MSTEP) * 16;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int r = m0 + g + (e >> 1) * 8, c = c0 + (e & 1);
+      if (r < nrows && c < wsz) Cv[r + c * ldc] = acc[i][e];
+    }
+  }
+}
+
 template <int NT>
 __device__ void apply_block_t(double *Ctop, double *Cv, int ldc, int nrows, const double *V, int ldv,
                               const double *Ts, int bw, int wsz, bool trans, double *W, double *W2) {
@@ -269,7 +302,7 @@ __device__ void apply_block_t(double *Ctop, double *Cv, int ldc, int nrows, cons
   // phase 1: W (bw x wsz) = V^T Cv, one 16x8 fragment per warp-iteration, full K in 4 chains
   {
     const int mt = (bw + 15) >> 4;
-    const int kpad = (nrows + 3) & ~3;
+    const int kpad = (nrows + 15) & ~15;        // V rows [nrows, kpad) are zero
     for (int f = warp; f < mt * nt; f += kWarps) {
       const int m0 = (f % mt) * 16, n0 = (f / mt) * 8;
       double acc[4][4];
@@ -280,14 +313,10 @@ __device__ void apply_block_t(double *Ctop, double *Cv, int ldc, int nrows, cons
       const double *va = V + (m0 + g) * ldv + t;
       const double *vb = va + 8 * ldv;
       const double *cb = Cv + (n0 + g) * ldc + t;
-      int k = 0;
-      for (; k + 16 <= kpad; k += 16) {
+      for (int k = 0; k < kpad; k += 16) {      // branch-free body: DMMAs under a branch do not overlap
 #pragma unroll
         for (int u = 0; u < 4; ++u) dmma(acc[u], va[k + 4 * u], vb[k + 4 * u], cb[k + 4 * u]);
       }
-#pragma unroll
-      for (int u = 0; u < 3; ++u)
-        if (k + 4 * u < kpad) dmma(acc[u], va[k + 4 * u], vb[k + 4 * u], cb[k + 4 * u]);
       const int r0 = m0 + g, c0 = n0 + 2 * t;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -306,22 +335,18 @@ __device__ void apply_block_t(double *Ctop, double *Cv, int ldc, int nrows, cons
   for (int f = warp; f < 2 * nt; f += kWarps) {
     const int m0 = (f & 1) * 16, n0 = (f >> 1) * 8;
     double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
-    for (int k = 0; k < kpad3; k += 8) {
+    // K = 32 always: T is zero beyond bw, so the padding adds exact zeros
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int kk = k + 4 * u;
-        if (kk < kpad3) {
-          double a0, a1;
-          if (trans) {   // A[l][m] = T[m][l]
-            a0 = Ts[(kk + t) + (m0 + g) * kTld];
-            a1 = Ts[(kk + t) + (m0 + g + 8) * kTld];
-          } else {       // A[l][m] = T[l][m]
-            a0 = Ts[(m0 + g) + (kk + t) * kTld];
-            a1 = Ts[(m0 + g + 8) + (kk + t) * kTld];
-          }
-          dmma(acc[u], a0, a1, W[(kk + t) + (n0 + g) * ldw]);
-        }
+    for (int kk = 0; kk < 32; kk += 4) {
+      double a0, a1;
+      if (trans) {   // A[l][m] = T[m][l]
+        a0 = Ts[(kk + t) + (m0 + g) * kTld];
+        a1 = Ts[(kk + t) + (m0 + g + 8) * kTld];
+      } else {       // A[l][m] = T[l][m]
+        a0 = Ts[(m0 + g) + (kk + t) * kTld];
+        a1 = Ts[(m0 + g + 8) + (kk + t) * kTld];
       }
+      dmma(acc[(kk >> 2) & 1], a0, a1, W[(kk + t) + (n0 + g) * ldw]);
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -331,46 +356,23 @@ __device__ void apply_block_t(double *Ctop, double *Cv, int ldc, int nrows, cons
   }
   __syncthreads();
   prof_mark(PH_TRI);
-  // phase 3: Cv (nrows x wsz) += V W2
+  // phase 3: Cv (nrows x wsz) += V W2, fragments dealt round-robin; the
+  // per-warp fragment count selects a static-trip-count instance
   {
-    constexpr int MSTEP = kWarps / NT;              // m-tile stride of a warp
-    constexpr int MF = (kMaxNb / 16 + MSTEP - 1) / MSTEP;   // max fragments per warp
+    constexpr int MSTEP = kWarps / NT;
     const int mt = (nrows + 15) >> 4;
     const int n = warp % NT, mfirst = warp / NT;
-    if (n < nt) {
-      const int c0 = n * 8 + 2 * t;
-      double acc[MF][4];
-#pragma unroll
-      for (int i = 0; i < MF; ++i) {
-        const int m0 = (mfirst + i * MSTEP) * 16;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int r = m0 + g + (e >> 1) * 8, c = c0 + (e & 1);
-          acc[i][e] = m0 < nrows ? Cv[r + c * ldc] : 0.0;
-        }
-      }
-      for (int k = 0; k < kpad3; k += 4) {
-        const double b = W2[(k + t) + (n * 8 + g) * ldw];
-#pragma unroll
-        for (int i = 0; i < MF; ++i) {
-          const int m = mfirst + i * MSTEP;
-          if (m < mt) {
-            const double a0 = V[(m * 16 + g) + (k + t) * ldv];
-            const double a1 = V[(m * 16 + g + 8) + (k + t) * ldv];
-            dmma(acc[i], a0, a1, b);
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < MF; ++i) {
-        const int m0 = (mfirst + i * MSTEP) * 16;
-        if (m0 < nrows) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int r = m0 + g + (e >> 1) * 8, c = c0 + (e & 1);
-            if (r < nrows && c < wsz) Cv[r + c * ldc] = acc[i][e];
-          }
-        }
+    const int nf = mt > mfirst ? (mt - mfirst + MSTEP - 1) / MSTEP : 0;
+    if (n < nt && nf > 0) {
+      switch (nf) {
+        case 1: phase3_frags<1, MSTEP>(Cv, ldc, nrows, V, ldv, W2, wsz, n, mfirst, kpad3); break;
+        case 2: phase3_frags<2, MSTEP>(Cv, ldc, nrows, V, ldv, W2, wsz, n, mfirst, kpad3); break;
+        case 3: phase3_frags<3, MSTEP>(Cv, ldc, nrows, V, ldv, W2, wsz, n, mfirst, kpad3); break;
+        case 4: phase3_frags<4, MSTEP>(Cv, ldc, nrows, V, ldv, W2, wsz, n, mfirst, kpad3); break;
+        case 5: phase3_frags<5, MSTEP>(Cv, ldc, nrows, V, ldv, W2, wsz, n, mfirst, kpad3); break;
+        case 6: phase3_frags<6, MSTEP>(Cv, ldc, nrows, V, ldv, W2, wsz, n, mfirst, kpad3); break;
+        case 7: phase3_frags<7, MSTEP>(Cv, ldc, nrows, V, ldv, W2, wsz, n, mfirst, kpad3); break;
+        default: phase3_frags<8, MSTEP>(Cv, ldc, nrows, V, ldv, W2, wsz, n, mfirst, kpad3); break;
       }
     }
   }
@@ -463,15 +465,13 @@ __device__ void gram_v(double *G, const double *V, int ldv, int nr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int m0 = (warp & 1) * 16, n0 = (warp >> 1) * 8;   // 8 warps = 2 x 4 fragments
-  const int kpad = (nr + 3) & ~3;
+  const int kpad = (nr + 15) & ~15;          // rows [nr, kpad) of V are zero
   double acc0[4] = {0.0, 0.0, 0.0, 0.0}, acc1[4] = {0.0, 0.0, 0.0, 0.0};
   const double *va = V + (m0 + g) * ldv + t, *vb = va + 8 * ldv, *vc = V + (n0 + g) * ldv + t;
-  int k = 0;
-  for (; k + 8 <= kpad; k += 8) {
+  for (int k = 0; k < kpad; k += 8) {
     dmma(acc0, va[k], vb[k], vc[k]);
     dmma(acc1, va[k + 4], vb[k + 4], vc[k + 4]);
   }
-  if (k < kpad) dmma(acc0, va[k], vb[k], vc[k]);
 #pragma unroll
   for (int e = 0; e < 4; ++e) G[(m0 + g + (e >> 1) * 8) + (n0 + 2 * t + (e & 1)) * kTld] = acc0[e] + acc1[e];
 }
