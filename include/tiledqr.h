@@ -158,6 +158,9 @@ int tiled_qr_host(int m, int n, int nb, int ib, int tree, int bs, int family,
  * (TQR_ECAP if cap < 16*n). */
 int tqr_trace_enable(int on);
 int64_t tqr_trace_fetch(uint64_t *out, int64_t cap);
+/* Successor lists (CSR, task ids in trace order) of the last traced plan:
+ * succ_ptr[ntask+1], succ[...]. Returns the number of edges or TQR_E*. */
+int64_t tqr_trace_graph(int32_t *succ_ptr, int32_t *succ, int64_t cap);
 
 /* Number of kernel launches the last device call issued (for bench accounting). */
 int tqr_last_launch_count(void);

@@ -40,6 +40,7 @@ _SIGS = {
     "tiled_qr_host": (ctypes.c_int, [ctypes.c_int] * 7 + [_VP, _VP, _VP]),
     "tqr_trace_enable": (ctypes.c_int, [ctypes.c_int]),
     "tqr_trace_fetch": (ctypes.c_int64, [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int64]),
+    "tqr_trace_graph": (ctypes.c_int64, [_I32P, _I32P, ctypes.c_int64]),
     "tqr_last_launch_count": (ctypes.c_int, []),
     "tqr_release_plans": (None, []),
     "tqr_last_error": (ctypes.c_char_p, []),
@@ -205,6 +206,15 @@ def trace_fetch():
     for x, p in enumerate(PHASES):
         out[f"c_{p}"] = r[:, 8 + x]
     return out
+
+
+def trace_graph(ntask: int):
+    """Successor CSR (ptr, idx) of the last traced plan (diagnostics)."""
+    cap = max(ntask + 1, 8 * ntask + 16)
+    ptr = np.zeros(cap, np.int32)
+    idx = np.zeros(cap, np.int32)
+    n = _check(lib().tqr_trace_graph(_ptr(ptr), _ptr(idx), cap))
+    return ptr[: ntask + 1].copy(), idx[:n].copy()
 
 
 def last_launch_count() -> int:

@@ -278,6 +278,23 @@ void build_apply_graph(const std::vector<TileTask> &tt, int p, int qc, int nb, i
   reorder(g, key, deps);
 }
 
+// Relative task durations for the bottom-level priorities (microseconds of the
+// B200 kernels on nb = 200 tiles, from the per-task tracer; only the ratios matter).
+static double est_duration(int kind) {
+  switch (kind) {
+    case K_GEQRT_B: case K_TTQRT_B: return 80;
+    case K_TSQRT_B: return 90;
+    case K_GEQRT_U: case K_TTQRT_U: case K_TSQRT_U: return 10;
+    case K_UNMQR: case K_AP_UNMQR: return 41;
+    case K_TTMQR: case K_AP_TTMQR: return 48;
+    case K_TSMQR: case K_AP_TSMQR: return 60;
+    case K_GEQRT: return 450;
+    case K_TTQRT: return 430;
+    case K_TSQRT: return 500;
+    default: return 40;
+  }
+}
+
 void finalize_dataflow(DevGraph &g, bool lookahead) {
   const int n = (int)g.tasks.size();
   std::vector<int32_t> cnt(n + 1, 0);
@@ -294,17 +311,21 @@ void finalize_dataflow(DevGraph &g, bool lookahead) {
   std::vector<char> chained(n, 0);
   for (int t = 0; t < n; ++t)
     if (g.tasks[t].chain >= 0) chained[g.tasks[t].chain] = 1;
+  // bottom level = longest estimated path from the task to the end (tasks are
+  // in a topological order); priority level = its quantised fraction of the max
+  std::vector<double> bl(n, 0.0);
+  double blmax = 1.0;
+  for (int t = n - 1; t >= 0; --t) {
+    double m = 0.0;
+    for (int x = cnt[t]; x < cnt[t + 1]; ++x) m = std::max(m, bl[g.succ[x]]);
+    bl[t] = est_duration(g.tasks[t].kind) + m;
+    blmax = std::max(blmax, bl[t]);
+  }
   for (int t = 0; t < n; ++t) {
     DevTask &x = g.tasks[t];
     const int indeg = x.dep_end - x.dep_begin;
-    // panel chain + look-ahead: the panels, the update of the next strip inside a
-    // split panel, and the updates of the next panel column (j = k+1)
-    const bool upd = x.kind == K_UNMQR || x.kind == K_TTMQR || x.kind == K_TSMQR;
-    const bool hi = x.kind == K_GEQRT || x.kind == K_TTQRT || x.kind == K_TSQRT || x.kind == K_GEQRT_B ||
-                    x.kind == K_TTQRT_B || x.kind == K_TSQRT_B ||
-                    ((x.kind == K_GEQRT_U || x.kind == K_TTQRT_U || x.kind == K_TSQRT_U) && x.s == x.j + 1) ||
-                    (lookahead && upd && x.j == x.k + 1);
-    x.meta = indeg | ((hi ? 1 : 0) << 16) | (chained[t] ? 1 << 17 : 0);
+    int level = lookahead ? std::min(kLevels - 1, (int)(kLevels * bl[t] / blmax)) : 0;
+    x.meta = indeg | (level << 16) | (chained[t] ? 1 << 20 : 0);
     x.dep_begin = cnt[t];
     x.dep_end = cnt[t + 1];
     if (indeg == 0) g.roots.push_back(t);

@@ -111,7 +111,7 @@ struct DevPlan {
   int32_t *succ = nullptr;
   int32_t *roots = nullptr;
   unsigned *cnt = nullptr;                // per-task arrivals (accumulate epoch x indegree)
-  unsigned long long *queue = nullptr;    // 2 x ntask ready-queue slots (epoch-tagged)
+  unsigned long long *queue = nullptr;    // kLevels x ntask ready-queue slots (epoch-tagged)
   int *ctrl = nullptr;                    // scheduler counters (kCtrlWords ints)
   unsigned long long *trace = nullptr;    // diagnostic per-task timestamps
   std::vector<DevTask> host_tasks;        // kept for tqr_trace_fetch
@@ -138,13 +138,13 @@ static int upload(const DevGraph &g, int ws, DevPlan &pl) {
   CUDA_TRY(cudaMalloc(&pl.succ, sizeof(int32_t) * (g.succ.empty() ? 1 : g.succ.size())));
   CUDA_TRY(cudaMalloc(&pl.roots, sizeof(int32_t) * (g.roots.empty() ? 1 : g.roots.size())));
   CUDA_TRY(cudaMalloc(&pl.cnt, sizeof(unsigned) * n1));
-  CUDA_TRY(cudaMalloc(&pl.queue, sizeof(unsigned long long) * 2 * n1));
+  CUDA_TRY(cudaMalloc(&pl.queue, sizeof(unsigned long long) * kLevels * n1));
   CUDA_TRY(cudaMalloc(&pl.ctrl, sizeof(int) * kCtrlWords));
   if (!g.tasks.empty()) CUDA_TRY(cudaMemcpy(pl.tasks, g.tasks.data(), sizeof(DevTask) * g.tasks.size(), cudaMemcpyHostToDevice));
   if (!g.succ.empty()) CUDA_TRY(cudaMemcpy(pl.succ, g.succ.data(), sizeof(int32_t) * g.succ.size(), cudaMemcpyHostToDevice));
   if (!g.roots.empty()) CUDA_TRY(cudaMemcpy(pl.roots, g.roots.data(), sizeof(int32_t) * g.roots.size(), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemset(pl.cnt, 0, sizeof(unsigned) * n1));
-  CUDA_TRY(cudaMemset(pl.queue, 0, sizeof(unsigned long long) * 2 * n1));
+  CUDA_TRY(cudaMemset(pl.queue, 0, sizeof(unsigned long long) * kLevels * n1));
   CUDA_TRY(cudaMemset(pl.ctrl, 0, sizeof(int) * kCtrlWords));
   return 0;
 }
@@ -182,6 +182,17 @@ extern "C" void tqr_release_plans(void) {
   std::lock_guard<std::mutex> lk(g_mu);
   g_plans.clear();
   g_trace_plan = nullptr;
+}
+
+extern "C" int64_t tqr_trace_graph(int32_t *succ_ptr, int32_t *succ, int64_t cap) {
+  DevPlan *pl = g_trace_plan;
+  if (!pl) return fail(TQR_EINVAL, "tqr_trace_graph: no traced launch");
+  int64_t ns = pl->host_tasks.empty() ? 0 : pl->host_tasks.back().dep_end;
+  if (cap < ns || cap < (int64_t)pl->ntask + 1) return fail(TQR_ECAP, "tqr_trace_graph: capacity too small");
+  for (int t = 0; t < pl->ntask; ++t) succ_ptr[t] = pl->host_tasks[t].dep_begin;
+  succ_ptr[pl->ntask] = (int32_t)ns;
+  if (ns) CUDA_TRY(cudaMemcpy(succ, pl->succ, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost));
+  return ns;
 }
 
 extern "C" int tqr_trace_enable(int on) {

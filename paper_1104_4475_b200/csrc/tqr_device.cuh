@@ -21,8 +21,10 @@ constexpr int kMaxIb = 32;
 constexpr size_t kMaxSmem = 227 * 1024 - 512;   // dynamic smem budget (opt-in max minus static)
 constexpr int kTld = 33;
 constexpr int kTraceWords = 12;             // per-task trace record (diagnostics)
-// scheduler control words (ints; each on its own 128-byte line)
-constexpr int kCtrlHead = 0, kCtrlTail = 32, kCtrlDone = 128, kCtrlExit = 160, kCtrlWords = 192;                    // ld of the 32 x 32 smem T / top / G blocks
+// scheduler control words (ints; each on its own 128-byte line): per priority
+// level l a queue head at kCtrlHead + 64 l and tail at kCtrlTail + 64 l
+constexpr int kCtrlHead = 0, kCtrlTail = 32, kCtrlDone = 64 * kLevels, kCtrlExit = 64 * kLevels + 32,
+              kCtrlWords = 64 * kLevels + 64;                    // ld of the 32 x 32 smem T / top / G blocks
 constexpr int kPanelScratch = 2 * 32 * kTld + 2 * 256 + 8 + 32;
 
 struct RunArgs {
@@ -32,7 +34,7 @@ struct RunArgs {
   int nroots;
   int ntask;
   unsigned *cnt;                // per-task arrivals, accumulated over launches (epoch * indegree when ready)
-  unsigned long long *queue;    // 2 ready queues of ntask slots: [0..ntask) panel chain, [ntask..2 ntask) others
+  unsigned long long *queue;    // kLevels ready queues of ntask slots each (level kLevels-1 = most critical)
   int *ctrl;                    // kCtrl* counters
   int epoch;
   int nctas;
@@ -273,14 +275,30 @@ __device__ __forceinline__ void phase3_frags(double *Cv, int ldc, int nrows, con
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[i][e] = Cv[(m0 + g + (e >> 1) * 8) + (c0 + (e & 1)) * ldc];
   }
-  for (int k = 0; k < kpad3; k += 4) {
-    const double b = W2[(k + t) + (n * 8 + g) * ldw];
+  // K = 32 always (W2 rows >= bw are exact zeros); loads of step k+4 overlap the DMMAs of step k
+  const double *wb = W2 + t + (n * 8 + g) * ldw;
+  const double *vr = V + g + t * ldv + mfirst * 16;
+  double b = wb[0], a0[NF], a1[NF];
+#pragma unroll
+  for (int i = 0; i < NF; ++i) { a0[i] = vr[i * MSTEP * 16]; a1[i] = vr[i * MSTEP * 16 + 8]; }
+#pragma unroll
+  for (int k = 4; k < 32; k += 4) {
+    const double nbv = wb[k];
+    double n0[NF], n1[NF];
 #pragma unroll
     for (int i = 0; i < NF; ++i) {
-      const int m0 = (mfirst + i * MSTEP) * 16;
-      dmma(acc[i], V[(m0 + g) + (k + t) * ldv], V[(m0 + g + 8) + (k + t) * ldv], b);
+      n0[i] = vr[i * MSTEP * 16 + k * ldv];
+      n1[i] = vr[i * MSTEP * 16 + 8 + k * ldv];
     }
+#pragma unroll
+    for (int i = 0; i < NF; ++i) dmma(acc[i], a0[i], a1[i], b);
+    b = nbv;
+#pragma unroll
+    for (int i = 0; i < NF; ++i) { a0[i] = n0[i]; a1[i] = n1[i]; }
   }
+#pragma unroll
+  for (int i = 0; i < NF; ++i) dmma(acc[i], a0[i], a1[i], b);
+  (void)kpad3;
 #pragma unroll
   for (int i = 0; i < NF; ++i) {
     const int m0 = (mfirst + i * MSTEP) * 16;
@@ -313,10 +331,22 @@ __device__ void apply_block_t(double *Ctop, double *Cv, int ldc, int nrows, cons
       const double *va = V + (m0 + g) * ldv + t;
       const double *vb = va + 8 * ldv;
       const double *cb = Cv + (n0 + g) * ldc + t;
-      for (int k = 0; k < kpad; k += 16) {      // branch-free body: DMMAs under a branch do not overlap
+      // branch-free, software-pipelined: the fragments of step k+16 are loaded
+      // while the DMMAs of step k run (DMMAs under a branch do not overlap)
+      double fa[4], fb[4], fc[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) dmma(acc[u], va[k + 4 * u], vb[k + 4 * u], cb[k + 4 * u]);
+      for (int u = 0; u < 4; ++u) { fa[u] = va[4 * u]; fb[u] = vb[4 * u]; fc[u] = cb[4 * u]; }
+      for (int k = 16; k < kpad; k += 16) {
+        double na[4], nb2[4], nc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { na[u] = va[k + 4 * u]; nb2[u] = vb[k + 4 * u]; nc[u] = cb[k + 4 * u]; }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma(acc[u], fa[u], fb[u], fc[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { fa[u] = na[u]; fb[u] = nb2[u]; fc[u] = nc[u]; }
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma(acc[u], fa[u], fb[u], fc[u]);
       const int r0 = m0 + g, c0 = n0 + 2 * t;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -887,15 +917,15 @@ __device__ __forceinline__ void st_release64(unsigned long long *p, unsigned lon
 }
 
 __device__ __forceinline__ void push_ready(const RunArgs &a, int t) {   // (chained tasks may be queued too)
-  const int q = (a.tasks[t].meta >> 16) & 1 ? 0 : 1;     // 0 = panel chain queue
-  const int pos = atomicAdd(&a.ctrl[kCtrlTail + 8 * q], 1);
+  const int q = (a.tasks[t].meta >> 16) & 15;
+  const int pos = atomicAdd(&a.ctrl[kCtrlTail + 64 * q], 1);
   st_release64(a.queue + (size_t)q * a.ntask + pos, ((unsigned long long)(unsigned)a.epoch << 32) | (unsigned)t);
 }
 
 // claim the next slot of queue q if one is published; returns the task or -1
 __device__ __forceinline__ int try_pop(const RunArgs &a, int q) {
-  int *head = &a.ctrl[kCtrlHead + 8 * q];
-  const int *tail = &a.ctrl[kCtrlTail + 8 * q];
+  int *head = &a.ctrl[kCtrlHead + 64 * q];
+  const int *tail = &a.ctrl[kCtrlTail + 64 * q];
   int h = ld_relaxed(head);
   while (h < ld_relaxed(tail)) {
     const int got = atomicCAS(head, h, h + 1);
@@ -917,7 +947,7 @@ __device__ __forceinline__ unsigned ld_acquire_u(const unsigned *p) {
 }
 __device__ __forceinline__ unsigned need_count(const RunArgs &a, int t) {
   const int m = a.tasks[t].meta;
-  return (unsigned)a.epoch * (unsigned)((m & 0xffff) + ((m >> 17) & 1));
+  return (unsigned)a.epoch * (unsigned)((m & 0xffff) + ((m >> 20) & 1));
 }
 __device__ __forceinline__ bool is_panel_block(int kind) {
   return kind == K_GEQRT_B || kind == K_TTQRT_B || kind == K_TSQRT_B;
@@ -940,9 +970,7 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
         s_resident = 0;
         for (;;) {
           if (ld_relaxed(&a.ctrl[kCtrlDone]) >= a.ntask) { t = -1; break; }
-          t = try_pop(a, 0);
-          if (t >= 0) break;
-          t = try_pop(a, 1);
+          for (int q = kLevels - 1; q >= 0 && t < 0; --q) t = try_pop(a, q);
           if (t >= 0) break;
           __nanosleep(64);
         }
@@ -994,8 +1022,7 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
   if (threadIdx.x == 0) {
     const int n = atomicAdd(&a.ctrl[kCtrlExit], 1);
     if (n == a.nctas - 1) {
-      a.ctrl[kCtrlHead] = 0; a.ctrl[kCtrlTail] = 0;
-      a.ctrl[kCtrlHead + 8] = 0; a.ctrl[kCtrlTail + 8] = 0;
+      for (int q = 0; q < kLevels; ++q) a.ctrl[kCtrlHead + 64 * q] = a.ctrl[kCtrlTail + 64 * q] = 0;
       a.ctrl[kCtrlDone] = 0; a.ctrl[kCtrlExit] = 0;
       __threadfence();
     }

@@ -60,3 +60,37 @@ for kd in np.unique(tr["kind"]):
 order = np.argsort(tr["ready"])
 first = (tr["ready"] - t0) / 1e3
 print(f"  tasks started in first 10% of span: {(first < 0.1 * span).sum()}, last 10%: {(first > 0.9 * span).sum()}")
+
+# critical path of the executed graph with the measured task durations (unbounded SMs)
+ptr, idx = tq.trace_graph(len(tr))
+dur = (tr["done"] - tr["ready"]) / 1e3
+fin = np.zeros(len(tr))
+start = np.zeros(len(tr))
+for t in range(len(tr)):          # tasks are in a topological order
+    fin[t] = start[t] + dur[t]
+    for x in range(ptr[t], ptr[t + 1]):
+        sc = idx[x]
+        if fin[t] > start[sc]:
+            start[sc] = fin[t]
+cp = fin.max()
+print(f"  critical path with measured durations: {cp / 1e3:.3f} ms (span {span / 1e3:.3f} ms, "
+      f"work/SMs {run.sum() / nsm / 1e3:.3f} ms)")
+# kinds on the critical path
+t = int(np.argmax(fin))
+path = []
+pred = {}
+for u in range(len(tr)):
+    for x in range(ptr[u], ptr[u + 1]):
+        sc = idx[x]
+        if abs(fin[u] - start[sc]) < 1e-9:
+            pred.setdefault(sc, u)
+while True:
+    path.append(t)
+    if t not in pred:
+        break
+    t = pred[t]
+kinds = {}
+for u in path:
+    k = tq.KIND_NAMES[tr["kind"][u]]
+    kinds[k] = kinds.get(k, 0) + dur[u]
+print("  critical path composition (ms): " + ", ".join(f"{k} {v / 1e3:.2f}" for k, v in sorted(kinds.items(), key=lambda x: -x[1])))
