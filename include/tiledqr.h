@@ -121,9 +121,9 @@ int64_t tiled_times(int p, int q, int tree, int bs, int family, int32_t *zero_ti
  *   nb     tile size, 1 <= nb <= 256;  ib  inner blocking, 1 <= ib <= 32
  *   A      device, p*q*nb*nb doubles in the tiled layout; overwritten by R/V
  *   T      device, p*q*2*ib*nb doubles; overwritten by the compact-WY factors
- * The whole factorization is ONE persistent kernel launch on `stream` (plus a
- * 4-byte memset of the task counter): every CTA pulls tasks in a topological
- * priority order and waits on per-task completion flags.
+ * The whole factorization is ONE persistent kernel launch on `stream`: a
+ * dataflow scheduler with per-task dependency counters and priority ready
+ * queues; every CTA only takes tasks whose inputs are complete.
  * Returns 0 or a negative TQR_E* code; asynchronous w.r.t. the host. */
 int tiled_qr(int m, int n, int nb, int ib, int tree, int bs, int family,
              double *A, double *T, void *stream);
