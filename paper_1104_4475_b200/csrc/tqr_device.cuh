@@ -553,84 +553,78 @@ __device__ void panel_block(double *X, double *A1, double *Tslot, int nb, int ib
   }
 
   double betas[4] = {0.0, 0.0, 0.0, 0.0};   // R diagonal of owned columns (lane c of owner)
+  // The column loop is unrolled over the owner's slot qo (c = 8 qo + wo) so the
+  // owner reads and writes its column with static register indices.
+#pragma unroll
+  for (int qo = 0; qo < 4; ++qo) {
 #pragma unroll 1
-  for (int c = 0; c < bw; ++c) {
-    const int qo = c >> 3, wo = c & 7;
-    const int pr = j0 + c;
-    double *vb = vsh + (c & 1) * 256;
-    PPROF(PH_STORE);
-    if (warp == wo) {
-      // ---- generate reflector c from the owned column a[qo][*] ----
-      double col[8];
+    for (int wo = 0; wo < 8; ++wo) {
+      const int c = 8 * qo + wo;
+      if (c >= bw) break;
+      const int pr = j0 + c;
+      double *vb = vsh + (c & 1) * 256;
+      if (warp == wo) {
+        // ---- generate reflector c from the owned column a[qo][*] ----
+        const int first = MODE == 0 ? c + 1 : 0;                 // first participating relative row
+        const int last = MODE == 1 ? pr : nr - 1;                // last participating relative row
+        double ss = 0.0;
 #pragma unroll
-      for (int s2 = 0; s2 < 8; ++s2)
-        col[s2] = qo == 0 ? a[0][s2] : (qo == 1 ? a[1][s2] : (qo == 2 ? a[2][s2] : a[3][s2]));
-      const double ptq = qo == 0 ? pt[0] : (qo == 1 ? pt[1] : (qo == 2 ? pt[2] : pt[3]));
-      const int first = MODE == 0 ? c + 1 : 0;                 // first participating relative row
-      const int last = MODE == 1 ? pr : nr - 1;                // last participating relative row
-      double ss = 0.0;
-#pragma unroll
-      for (int s2 = 0; s2 < 8; ++s2) {
-        const int rr = lane + 32 * s2;
-        if (rr >= first && rr <= last) ss = fma(col[s2], col[s2], ss);
-      }
-      const double xn2 = warp_sum(ss);
-      PPROF(PH_LOAD);
-      const double alpha = __shfl_sync(0xffffffffu, MODE == 0 ? col[0] : ptq, c);
-      double beta, tau, scale;
-      larfg_scalars(alpha, xn2, beta, tau, scale);
-      PPROF(PH_FIX);
-#pragma unroll
-      for (int s2 = 0; s2 < 8; ++s2) {
-        const int rr = lane + 32 * s2;
-        const double v = (rr >= first && rr <= last) ? scale * col[s2] : 0.0;
-        vb[rr] = v;
-        if (rr >= first && rr <= last) col[s2] = v;               // column now holds V below the pivot
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (q == qo) {
-#pragma unroll
-          for (int s2 = 0; s2 < 8; ++s2) a[q][s2] = col[s2];
-          if (lane == c) betas[q] = beta;
+        for (int s2 = 0; s2 < 8; ++s2) {
+          const int rr = lane + 32 * s2;
+          if (rr >= first && rr <= last) ss = fma(a[qo][s2], a[qo][s2], ss);
         }
-      if (lane == 0) { scal[(c & 1) * 4] = tau; taus[c] = tau; }
-      PPROF(PH_MMA1);
-    }
-    __syncthreads();
-    PPROF(PH_TRI);
-    // ---- apply reflector c to the owned columns > c ----
-    // branch-free over the 4 owned columns so the 4 warp reductions overlap
-    const double tau = scal[(c & 1) * 4];
-    if (warp + 8 * 3 > c && tau != 0.0) {
-      double v[8];
+        const double xn2 = warp_sum(ss);
+        const double alpha = __shfl_sync(0xffffffffu, MODE == 0 ? a[qo][0] : pt[qo], c);
+        double beta, tau, scale;
+        larfg_scalars(alpha, xn2, beta, tau, scale);
 #pragma unroll
-      for (int s2 = 0; s2 < 8; ++s2) v[s2] = vb[lane + 32 * s2];
-      double d[4], P[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        d[q] = 0.0;
-#pragma unroll
-        for (int s2 = 0; s2 < 8; ++s2) d[q] = fma(v[s2], a[q][s2], d[q]);
-        P[q] = MODE == 0 ? __shfl_sync(0xffffffffu, a[q][0], c) : __shfl_sync(0xffffffffu, pt[q], c);
+        for (int s2 = 0; s2 < 8; ++s2) {
+          const int rr = lane + 32 * s2;
+          const bool tl = rr >= first && rr <= last;
+          const double v = tl ? scale * a[qo][s2] : 0.0;
+          vb[rr] = v;
+          if (tl) a[qo][s2] = v;               // column now holds V below the pivot
+        }
+        if (lane == c) betas[qo] = beta;
+        if (lane == 0) { scal[(c & 1) * 4] = tau; taus[c] = tau; }
       }
+      __syncthreads();
+      // ---- apply reflector c to the owned columns > c ----
+      // branch-free over the 4 owned columns so the 4 warp reductions overlap
+      const double tau = scal[(c & 1) * 4];
+      if (warp + 8 * 3 > c && tau != 0.0) {
+        double v[8];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
+        for (int s2 = 0; s2 < 8; ++s2) v[s2] = vb[lane + 32 * s2];
+        double d[4], P[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) d[q] += __shfl_xor_sync(0xffffffffu, d[q], o);
+        for (int q = 0; q < 4; ++q) {
+          d[q] = 0.0;
+          if (q >= qo) {               // slots below qo hold finished columns (static skip)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int cl = warp + 8 * q;
-        const double tw = (cl > c && cl < bw) ? tau * (P[q] + d[q]) : 0.0;
+            for (int s2 = 0; s2 < 8; ++s2) d[q] = fma(v[s2], a[q][s2], d[q]);
+          }
+          P[q] = MODE == 0 ? __shfl_sync(0xffffffffu, a[q][0], c) : __shfl_sync(0xffffffffu, pt[q], c);
+        }
 #pragma unroll
-        for (int s2 = 0; s2 < 8; ++s2) a[q][s2] = fma(-tw, v[s2], a[q][s2]);
-        if (lane == c) {
-          if (MODE == 0) a[q][0] -= tw;
-          else pt[q] -= tw;
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q >= qo) d[q] += __shfl_xor_sync(0xffffffffu, d[q], o);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (q < qo) continue;
+          const int cl = warp + 8 * q;
+          const double tw = (cl > c && cl < bw) ? tau * (P[q] + d[q]) : 0.0;
+#pragma unroll
+          for (int s2 = 0; s2 < 8; ++s2) a[q][s2] = fma(-tw, v[s2], a[q][s2]);
+          if (lane == c) {
+            if (MODE == 0) a[q][0] -= tw;
+            else pt[q] -= tw;
+          }
         }
       }
     }
-    PPROF(PH_MMA3);
   }
   // ---- write back the owned columns: X (R above / V below the pivot) and Vbuf ----
 #pragma unroll

@@ -94,3 +94,20 @@ for u in path:
     k = tq.KIND_NAMES[tr["kind"][u]]
     kinds[k] = kinds.get(k, 0) + dur[u]
 print("  critical path composition (ms): " + ", ".join(f"{k} {v / 1e3:.2f}" for k, v in sorted(kinds.items(), key=lambda x: -x[1])))
+# utilisation over time (busy SMs per 5% of the span) and what runs
+nb_ = 20
+edges = np.linspace(0, span, nb_ + 1)
+rs, rd = (tr["ready"] - t0) / 1e3, (tr["done"] - t0) / 1e3
+util = []
+for b in range(nb_):
+    lo, hi = edges[b], edges[b + 1]
+    ov = np.clip(np.minimum(rd, hi) - np.maximum(rs, lo), 0, None)
+    util.append(ov.sum() / ((hi - lo) * nsm))
+print("  busy fraction per 5% of span: " + " ".join(f"{u:.2f}" for u in util))
+panel = np.isin(tr["kind"], [9, 11, 13])
+cpb = []
+for b in range(nb_):
+    lo, hi = edges[b], edges[b + 1]
+    ov = np.clip(np.minimum(rd, hi) - np.maximum(rs, lo), 0, None)
+    cpb.append((ov * panel).sum() / (hi - lo))
+print("  concurrent panel tasks per 5%:   " + " ".join(f"{u:4.1f}" for u in cpb))
