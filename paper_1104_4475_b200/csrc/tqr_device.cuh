@@ -157,17 +157,13 @@ __device__ __forceinline__ void async_block(double *dst, int lds, const double *
   if (nr <= 0 || ncol <= 0) return;
   const double *g = src + r0 + (size_t)c0 * ldg;
   const bool v16 = ((nr | lds | ldg) & 1) == 0 && ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
-  if (v16) {
-    const int h = nr >> 1;
-    for (int idx = threadIdx.x; idx < h * ncol; idx += kThreads) {
-      const int r = (idx % h) * 2, c = idx / h;
-      cp_async16(dst + r + c * lds, g + r + (size_t)c * ldg);
-    }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (v16) {          // warps over columns, lanes over 16-byte row pairs (no integer division)
+    for (int c = warp; c < ncol; c += kWarps)
+      for (int r = 2 * lane; r < nr; r += 64) cp_async16(dst + r + c * lds, g + r + (size_t)c * ldg);
   } else {
-    for (int idx = threadIdx.x; idx < nr * ncol; idx += kThreads) {
-      const int r = idx % nr, c = idx / nr;
-      cp_async8(dst + r + c * lds, g + r + (size_t)c * ldg);
-    }
+    for (int c = warp; c < ncol; c += kWarps)
+      for (int r = lane; r < nr; r += 32) cp_async8(dst + r + c * lds, g + r + (size_t)c * ldg);
   }
 }
 
@@ -178,19 +174,15 @@ __device__ __forceinline__ void load_rows(double *buf, int ldc, int off, const d
 }
 __device__ __forceinline__ void store_rows(const double *buf, int ldc, int off, double *tile, int nb,
                                            int r0, int r1, int c0, int wsz) {
-  const int nr = r1 - r0;
-  if (((nr | ldc | nb | r0 | off) & 1) == 0) {
-    const int h = nr >> 1;
-    for (int idx = threadIdx.x; idx < h * wsz; idx += kThreads) {
-      const int r = r0 + (idx % h) * 2, c = idx / h;
-      *reinterpret_cast<double2 *>(tile + r + (size_t)(c0 + c) * nb) =
-          *reinterpret_cast<const double2 *>(buf + off + r + c * ldc);
-    }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if ((((r1 - r0) | ldc | nb | r0 | off) & 1) == 0) {
+    for (int c = warp; c < wsz; c += kWarps)
+      for (int r = r0 + 2 * lane; r < r1; r += 64)
+        *reinterpret_cast<double2 *>(tile + r + (size_t)(c0 + c) * nb) =
+            *reinterpret_cast<const double2 *>(buf + off + r + c * ldc);
   } else {
-    for (int idx = threadIdx.x; idx < nr * wsz; idx += kThreads) {
-      int r = r0 + idx % nr, c = idx / nr;
-      tile[r + (size_t)(c0 + c) * nb] = buf[off + r + c * ldc];
-    }
+    for (int c = warp; c < wsz; c += kWarps)
+      for (int r = r0 + lane; r < r1; r += 32) tile[r + (size_t)(c0 + c) * nb] = buf[off + r + c * ldc];
   }
 }
 
@@ -202,12 +194,17 @@ __device__ __forceinline__ void issue_v_geqrt(double *V, int ldv, const double *
 }
 __device__ __forceinline__ void fix_v_geqrt(double *V, int ldv, int nb, int j0, int bw) {
   const int nr = nb - j0, nr4 = (nr + 15) & ~15;
-  for (int idx = threadIdx.x; idx < bw * bw; idx += kThreads) {
-    const int rr = idx % bw, l = idx / bw;
-    if (rr <= l && rr < nr) V[rr + l * ldv] = rr == l ? 1.0 : 0.0;
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int l = warp; l < bw; l += kWarps)
+      if (lane <= l && lane < nr) V[lane + l * ldv] = lane == l ? 1.0 : 0.0;
   }
   const int pad = nr4 - nr;
-  for (int idx = threadIdx.x; idx < pad * bw; idx += kThreads) V[nr + idx % pad + (idx / pad) * ldv] = 0.0;
+  if (pad > 0) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int l = warp; l < bw; l += kWarps)
+      if (lane < pad) V[nr + lane + l * ldv] = 0.0;
+  }
 }
 // V2 of a TTQRT (tri) / TSQRT block: rows 0..R2-1 of tile X, R2 = j0+bw (TT) or nb (TS);
 // in TT only the upper triangle (r <= j0+l) belongs to the reflectors.
@@ -217,26 +214,33 @@ __device__ __forceinline__ void issue_v_tp(double *V, int ldv, const double *X, 
 __device__ __forceinline__ void fix_v_tp(double *V, int ldv, int nb, int j0, int bw, bool tri) {
   const int nr = tri ? j0 + bw : nb, nr4 = (nr + 15) & ~15;
   if (tri) {
-    for (int idx = threadIdx.x; idx < bw * bw; idx += kThreads) {
-      const int rr = idx % bw, l = idx / bw;
-      if (rr > l) V[j0 + rr + l * ldv] = 0.0;
-    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int l = warp; l < bw; l += kWarps)
+      if (lane > l && lane < bw) V[j0 + lane + l * ldv] = 0.0;
   }
   const int pad = nr4 - nr;
-  for (int idx = threadIdx.x; idx < pad * bw; idx += kThreads) V[nr + idx % pad + (idx / pad) * ldv] = 0.0;
+  if (pad > 0) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int l = warp; l < bw; l += kWarps)
+      if (lane < pad) V[nr + lane + l * ldv] = 0.0;
+  }
 }
 // zero V rows [nr, round_up(nr, 16)) of columns 0..bw-1 (K padding of the DMMA loops)
 __device__ __forceinline__ void zero_vpad(double *V, int ldv, int nr, int bw) {
   const int pad = ((nr + 15) & ~15) - nr;
-  for (int idx = threadIdx.x; idx < pad * bw; idx += kThreads) V[nr + idx % pad + (idx / pad) * ldv] = 0.0;
+  if (pad > 0) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int l = warp; l < bw; l += kWarps)
+      if (lane < pad) V[nr + lane + l * ldv] = 0.0;
+  }
 }
 // T block (bw x bw upper triangular) of columns j0.. of a T slot -> Ts (ld kTld);
 // the rest of the 32 x 32 block is zeroed (it feeds a padded DMMA)
 __device__ __forceinline__ void issue_t(double *Ts, const double *Tslot, int ib, int j0, int bw) {
-  for (int idx = threadIdx.x; idx < 32 * 32; idx += kThreads) {
-    const int l = idx & 31, c = idx >> 5;
-    if (l <= c && c < bw) cp_async8(Ts + l + c * kTld, Tslot + l + (size_t)(j0 + c) * ib);
-    else Ts[l + c * kTld] = 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = warp; c < 32; c += kWarps) {
+    if (lane <= c && c < bw) cp_async8(Ts + lane + c * kTld, Tslot + lane + (size_t)(j0 + c) * ib);
+    else Ts[lane + c * kTld] = 0.0;
   }
 }
 
@@ -407,10 +411,8 @@ __device__ void apply_block_t(double *Ctop, double *Cv, int ldc, int nrows, cons
     }
   }
   if (Ctop) {
-    for (int idx = threadIdx.x; idx < bw * wsz; idx += kThreads) {
-      const int l = idx % bw, c = idx / bw;
-      Ctop[l + c * ldc] += W2[l + c * ldw];
-    }
+    for (int c = warp; c < wsz; c += kWarps)
+      if (lane < bw) Ctop[lane + c * ldc] += W2[lane + c * ldw];
   }
   __syncthreads();
   prof_mark(PH_MMA3);
@@ -668,10 +670,8 @@ __device__ void panel_block(double *X, double *A1, double *Tslot, int nb, int ib
   __syncthreads();
   t_doubling(Ts, G, top);
   prof_mark(PH_TREC);
-  for (int idx = tid; idx < ib * bw; idx += kThreads) {
-    int l = idx % ib, c = idx / ib;
-    Tslot[l + (size_t)(j0 + c) * ib] = (l < bw && l <= c) ? Ts[l + c * kTld] : 0.0;
-  }
+  for (int c = warp; c < bw; c += kWarps)
+    if (lane < ib) Tslot[lane + (size_t)(j0 + c) * ib] = (lane < bw && lane <= c) ? Ts[lane + c * kTld] : 0.0;
 }
 
 // ---- panel kernels: GEQRT / TTQRT / TSQRT on whole tiles ------------------
