@@ -40,6 +40,7 @@ struct RunArgs {
   int nctas;
   double *A, *T, *C;
   int p, q, nb, ib, ws, trans;
+  int tma;                     // 1: move C strips and V blocks with 1-D TMA bulk copies
   unsigned long long *trace;   // optional: kTraceWords u64 per task (taken, ready, done, smid<<32|kind, 8 phase cycle counters)
 };
 
@@ -149,6 +150,8 @@ __device__ __forceinline__ void cp_async16(double *dst, const double *src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+
+
 // copy rows [r0, r1) of columns [c0, c0+ncol) of a column-major global array
 // (leading dimension ldg) to shared dst[(r - r0) + c*lds]
 __device__ __forceinline__ void async_block(double *dst, int lds, const double *src, int ldg, int r0, int r1,
@@ -160,11 +163,72 @@ __device__ __forceinline__ void async_block(double *dst, int lds, const double *
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (v16) {          // warps over columns, lanes over 16-byte row pairs (no integer division)
     for (int c = warp; c < ncol; c += kWarps)
-      for (int r = 2 * lane; r < nr; r += 64) cp_async16(dst + r + c * lds, g + r + (size_t)c * ldg);
+      for (int r = 2 * lane; r < nr; r += 64) cp_async16(dst + r + c * lds, g + r + (size_t)c * ldg);   // dst row 0 = r0
   } else {
     for (int c = warp; c < ncol; c += kWarps)
       for (int r = lane; r < nr; r += 32) cp_async8(dst + r + c * lds, g + r + (size_t)c * ldg);
   }
+}
+
+// ---- TMA (1-D bulk copies) with an mbarrier transaction count --------------
+// One cp.async.bulk per tile column (global column segment -> smem column),
+// issued by the lanes of warp 0; completion is tracked by the CTA's mbarrier
+// (expect_tx per issue, one arrival per batch, parity wait). The SASS shows
+// UBLKCP. Sizes/addresses that are not 16-byte multiples fall back to cp.async.
+__shared__ __align__(8) unsigned long long s_mbar;
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init() {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_mbar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// issue column copies rows [r0, r1) of columns [c0, c0+ncol): TMA when every
+// column segment is 16-byte aligned and a multiple of 16 bytes, else cp.async
+__device__ __forceinline__ void tma_block(double *dst, int lds, const double *src, int ldg, int r0, int r1,
+                                          int c0, int ncol, bool use_tma) {
+  const int nr = r1 - r0;
+  if (nr <= 0 || ncol <= 0) return;
+  const double *g = src + r0 + (size_t)c0 * ldg;
+  const bool ok = use_tma && ((nr | lds | ldg) & 1) == 0 &&
+                  ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  if (!ok) {
+    async_block(dst, lds, src, ldg, r0, r1, c0, ncol);
+    return;
+  }
+  if (threadIdx.x < 32) {
+    const unsigned bytes = (unsigned)nr * 8u;
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async;" ::: "memory");
+      asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_mbar)),
+                   "r"(bytes * (unsigned)ncol) : "memory");
+    }
+    __syncwarp();
+    for (int c = threadIdx.x; c < ncol; c += 32)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(dst + c * lds)), "l"(g + (size_t)c * ldg), "r"(bytes), "r"(smem_u32(&s_mbar))
+                   : "memory");
+  }
+}
+
+// wait for every outstanding copy of this batch: cp.async groups and the TMA
+// transactions (one arrival + parity wait; `phase` is the per-thread parity)
+__device__ __forceinline__ void async_wait(unsigned &phase) {
+  cp_async_wait_all();
+  if (threadIdx.x == 0) {
+    unsigned long long st;
+    asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(st) : "r"(smem_u32(&s_mbar)) : "memory");
+  }
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "TQR_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra TQR_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(&s_mbar)), "r"(phase) : "memory");
+  phase ^= 1u;
 }
 
 // ---- strip movement: rows [r0, r1) of tile columns [c0, c0+wsz) <-> buf rows (off + r)
@@ -717,22 +781,22 @@ __device__ void panel_task(double *X, double *A1, double *Tslot, int nb, int ib,
 // GEQRT reflectors of tile Vt; only rows >= b_lo*ib are touched.
 __device__ void unmqr_strip(const double *Vt, const double *Tslot, double *Ct, int nb, int ib, int cs,
                             int wsz, bool trans, int b_lo, int b_hi, double *smem, const SmemLayout &L,
-                            bool resident = false) {
+                            unsigned &mbph, bool tma, bool resident = false) {
   double *Cb = smem + L.offC, *Wb = smem + L.offW;
   const int r0 = b_lo * ib;
   const int nblk = b_hi - b_lo;
   auto blk = [&](int idx) { return trans ? b_lo + idx : b_hi - 1 - idx; };
-  load_rows(Cb, L.ldc, 0, Ct, nb, r0, nb, cs, wsz);
+  tma_block(Cb + r0, L.ldc, Ct, nb, r0, nb, cs, wsz, tma);
   if (!resident) {     // resident: the panel task just left V (unit diagonal, padded) and T in buffer 0
     const int j0 = blk(0) * ib, bw = min(ib, nb - j0);
-    issue_v_geqrt(smem + L.offV[0], L.ldv, Vt, nb, j0, bw);
+    tma_block(smem + L.offV[0], L.ldv, Vt, nb, j0, nb, j0, bw, tma);
     issue_t(smem + L.offT[0], Tslot, ib, j0, bw);
   }
   for (int idx = 0; idx < nblk; ++idx) {
     const int cur = idx & (L.nvb - 1);
     double *Vb = smem + (cur ? L.offV[1] : L.offV[0]), *Ts = smem + (cur ? L.offT[1] : L.offT[0]);
     const int j0 = blk(idx) * ib, bw = min(ib, nb - j0);
-    cp_async_wait_all();
+    async_wait(mbph);
     __syncthreads();
     prof_mark(PH_LOAD);
     if (!(resident && idx == 0)) {
@@ -742,13 +806,13 @@ __device__ void unmqr_strip(const double *Vt, const double *Tslot, double *Ct, i
     prof_mark(PH_FIX);
     if (L.nvb == 2 && idx + 1 < nblk) {
       const int j1 = blk(idx + 1) * ib, bw1 = min(ib, nb - j1);
-      issue_v_geqrt(smem + (cur ? L.offV[0] : L.offV[1]), L.ldv, Vt, nb, j1, bw1);
+      tma_block(smem + (cur ? L.offV[0] : L.offV[1]), L.ldv, Vt, nb, j1, nb, j1, bw1, tma);
       issue_t(smem + (cur ? L.offT[0] : L.offT[1]), Tslot, ib, j1, bw1);
     }
     apply_block(nullptr, Cb + j0, L.ldc, nb - j0, Vb, L.ldv, Ts, bw, wsz, trans, Wb, Wb + L.ldw * L.wcols);
     if (L.nvb == 1 && idx + 1 < nblk) {
       const int j1 = blk(idx + 1) * ib, bw1 = min(ib, nb - j1);
-      issue_v_geqrt(Vb, L.ldv, Vt, nb, j1, bw1);
+      tma_block(Vb, L.ldv, Vt, nb, j1, nb, j1, bw1, tma);
       issue_t(Ts, Tslot, ib, j1, bw1);
     }
   }
@@ -761,25 +825,25 @@ __device__ void unmqr_strip(const double *Vt, const double *Tslot, double *Ct, i
 // 0 .. (tri ? b*ib+bw : nb)-1 (resident).
 __device__ void tpmqr_strip(const double *Vt, const double *Tslot, double *C1, double *C2, int nb, int ib,
                             int cs, int wsz, bool tri, bool trans, int b_lo, int b_hi, double *smem,
-                            const SmemLayout &L, bool resident = false) {
+                            const SmemLayout &L, unsigned &mbph, bool tma, bool resident = false) {
   double *Cb = smem + L.offC, *Wb = smem + L.offW;
   const int r2hi = tri ? min(b_hi * ib, nb) : nb;
   const int nblk = b_hi - b_lo;
   auto blk = [&](int idx) { return trans ? b_lo + idx : b_hi - 1 - idx; };
-  load_rows(Cb, L.ldc, kWinRows, C2, nb, 0, r2hi, cs, wsz);
+  tma_block(Cb + kWinRows, L.ldc, C2, nb, 0, r2hi, cs, wsz, tma);
   {
     const int j0 = blk(0) * ib, bw = min(ib, nb - j0);
     if (!resident) {
-      issue_v_tp(smem + L.offV[0], L.ldv, Vt, nb, j0, bw, tri);
+      tma_block(smem + L.offV[0], L.ldv, Vt, nb, 0, tri ? j0 + bw : nb, j0, bw, tma);
       issue_t(smem + L.offT[0], Tslot, ib, j0, bw);
     }
-    async_block(Cb, L.ldc, C1, nb, j0, j0 + bw, cs, wsz);
+    tma_block(Cb, L.ldc, C1, nb, j0, j0 + bw, cs, wsz, tma);
   }
   for (int idx = 0; idx < nblk; ++idx) {
     const int cur = idx & (L.nvb - 1);
     double *Vb = smem + (cur ? L.offV[1] : L.offV[0]), *Ts = smem + (cur ? L.offT[1] : L.offT[0]), *win = Cb + 32 * (idx & 1);
     const int j0 = blk(idx) * ib, bw = min(ib, nb - j0);
-    cp_async_wait_all();
+    async_wait(mbph);
     __syncthreads();
     prof_mark(PH_LOAD);
     if (!(resident && idx == 0)) {
@@ -789,9 +853,9 @@ __device__ void tpmqr_strip(const double *Vt, const double *Tslot, double *C1, d
     prof_mark(PH_FIX);
     if (L.nvb == 2 && idx + 1 < nblk) {
       const int j1 = blk(idx + 1) * ib, bw1 = min(ib, nb - j1);
-      issue_v_tp(smem + (cur ? L.offV[0] : L.offV[1]), L.ldv, Vt, nb, j1, bw1, tri);
+      tma_block(smem + (cur ? L.offV[0] : L.offV[1]), L.ldv, Vt, nb, 0, tri ? j1 + bw1 : nb, j1, bw1, tma);
       issue_t(smem + (cur ? L.offT[0] : L.offT[1]), Tslot, ib, j1, bw1);
-      async_block(Cb + 32 * ((idx + 1) & 1), L.ldc, C1, nb, j1, j1 + bw1, cs, wsz);
+      tma_block(Cb + 32 * ((idx + 1) & 1), L.ldc, C1, nb, j1, j1 + bw1, cs, wsz, tma);
     }
     apply_block(win, Cb + kWinRows, L.ldc, tri ? j0 + bw : nb, Vb, L.ldv, Ts, bw, wsz, trans, Wb,
                 Wb + L.ldw * L.wcols);
@@ -799,15 +863,17 @@ __device__ void tpmqr_strip(const double *Vt, const double *Tslot, double *C1, d
     if (L.nvb == 1 && idx + 1 < nblk) {
       __syncthreads();
       const int j1 = blk(idx + 1) * ib, bw1 = min(ib, nb - j1);
-      issue_v_tp(Vb, L.ldv, Vt, nb, j1, bw1, tri);
+      tma_block(Vb, L.ldv, Vt, nb, 0, tri ? j1 + bw1 : nb, j1, bw1, tma);
       issue_t(Ts, Tslot, ib, j1, bw1);
-      async_block(Cb + 32 * ((idx + 1) & 1), L.ldc, C1, nb, j1, j1 + bw1, cs, wsz);
+      tma_block(Cb + 32 * ((idx + 1) & 1), L.ldc, C1, nb, j1, j1 + bw1, cs, wsz, tma);
     }
   }
   store_rows(Cb, L.ldc, kWinRows, C2, nb, 0, r2hi, cs, wsz);
 }
 
-__device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const SmemLayout &L, bool resident) {
+__device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const SmemLayout &L, bool resident,
+                         unsigned &mbph) {
+  const bool tma = a.tma != 0;
   const int p = a.p, nb = a.nb, ib = a.ib, ws = a.ws;
   const int nblk = (nb + ib - 1) / ib;
   double *Vb = smem + L.offV[0], *Wb = smem + L.offW, *Ts = smem + L.offT[0];
@@ -844,7 +910,7 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
       const int cs = t.s * ws, wsz = min(ws, nb - cs);
       double *X = tile_ptr(a.A, p, nb, t.i, t.k);
       unmqr_strip(X, tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0), X, nb, ib, cs, wsz, true, t.j, t.j + 1, smem, L,
-                  resident);
+                  mbph, tma, resident);
       break;
     }
     case K_TTQRT_U:
@@ -852,7 +918,7 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
       const int cs = t.s * ws, wsz = min(ws, nb - cs);
       double *X = tile_ptr(a.A, p, nb, t.i, t.k);
       tpmqr_strip(X, tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1), tile_ptr(a.A, p, nb, t.piv, t.k), X, nb, ib, cs, wsz,
-                  t.kind == K_TTQRT_U, true, t.j, t.j + 1, smem, L, resident);
+                  t.kind == K_TTQRT_U, true, t.j, t.j + 1, smem, L, mbph, tma, resident);
       break;
     }
     // ---- updates of other tiles (factorization) and of C (apply)
@@ -861,7 +927,7 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
       double *Cbase = t.kind == K_UNMQR ? a.A : a.C;
       const int cs = t.s * ws, wsz = min(ws, nb - cs);
       unmqr_strip(tile_ptr(a.A, p, nb, t.i, t.k), tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0),
-                  tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs, wsz, a.trans != 0, 0, nblk, smem, L);
+                  tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs, wsz, a.trans != 0, 0, nblk, smem, L, mbph, tma);
       break;
     }
     case K_TTMQR:
@@ -874,7 +940,7 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
       const int cs = t.s * ws, wsz = min(ws, nb - cs);
       tpmqr_strip(tile_ptr(a.A, p, nb, t.i, t.k), tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1),
                   tile_ptr(Cbase, p, nb, t.piv, t.j), tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs, wsz, tri,
-                  a.trans != 0, 0, nblk, smem, L);
+                  a.trans != 0, 0, nblk, smem, L, mbph, tma);
       break;
     }
     default:
@@ -951,7 +1017,8 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_task, s_chain, s_resident;
   const SmemLayout L = smem_layout(a.nb, a.ib, a.ws);
-  if (threadIdx.x == 0) { s_prof_on = 0; s_chain = -1; s_resident = 0; }
+  if (threadIdx.x == 0) { s_prof_on = 0; s_chain = -1; s_resident = 0; mbar_init(); }
+  unsigned mbph = 0u;   // parity of the CTA mbarrier (identical in every thread)
   // everything the DMMA padding may read must be finite: start from zeros
   for (size_t x = threadIdx.x; x < L.total; x += kThreads) smem[x] = 0.0;
   if (threadIdx.x == 0)
@@ -983,7 +1050,7 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
     if (t < 0) break;
     __threadfence();
     const DevTask tk = a.tasks[t];
-    run_task(a, tk, smem, L, s_resident != 0);
+    run_task(a, tk, smem, L, s_resident != 0, mbph);
     __syncthreads();
     prof_mark(PH_STORE);
     if (threadIdx.x == 0) {

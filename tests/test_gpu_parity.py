@@ -219,3 +219,15 @@ def test_tall_skinny_domains_on_one_gpu(world, tree):
     R = np.triu(qrinputs.from_tiles(Rs[0].cpu().numpy(), q, q, nb))
     Rl = np.linalg.qr(A, mode="r")
     assert rel(nu.sign_normalise(R), nu.sign_normalise(Rl)) <= TOL_R
+
+
+@pytest.mark.parametrize("tree,family", [("greedy", "TT"), ("flat", "TS")])
+def test_tma_bulk_copy_path(tree, family, monkeypatch):
+    """TQR_TMA=1 moves C strips and V blocks with 1-D TMA bulk copies
+    (cp.async.bulk + mbarrier); results equal the oracle as on the default path."""
+    monkeypatch.setenv("TQR_TMA", "1")
+    for (p, q, nb, ib) in [(4, 2, 72, 32), (3, 3, 64, 32), (6, 3, 20, 8)]:
+        A = qrinputs.gaussian(p * nb, q * nb, 123 + p)
+        compare_with_oracle(A, nb, ib, tree, 1, family)
+    A = qrinputs.gaussian(8 * 64, 3 * 64, 7)
+    compare_with_oracle(A, 64, 32, "plasma", 3, "TT")
