@@ -231,3 +231,45 @@ def test_tma_bulk_copy_path(tree, family, monkeypatch):
         compare_with_oracle(A, nb, ib, tree, 1, family)
     A = qrinputs.gaussian(8 * 64, 3 * 64, 7)
     compare_with_oracle(A, 64, 32, "plasma", 3, "TT")
+
+
+def test_config2_square_full_size():
+    """configs[2]: 8000 x 8000 (p = q = 40, nb = 200), Greedy. Checked on the device
+    (cuBLAS fp64 matmuls of the test only): ||A - QR|| / ||A||, ||I - Q^T Q||, and
+    R against LAPACK's R after row-sign normalisation."""
+    p = q = 40
+    nb, ib = 200, 32
+    m = n = p * nb
+    g = torch.Generator(device=DEV).manual_seed(77)
+    A = torch.randn(m, n, dtype=torch.float64, device=DEV, generator=g)
+    buf = tq.to_tiled(A, nb)
+    T = tq.tiled_qr(buf, m, n, nb, ib, "greedy")
+    R = torch.triu(tq.from_tiled(buf, m, n, nb))
+    Qb = tq.to_tiled(torch.eye(m, dtype=torch.float64, device=DEV), nb)
+    tq.apply_q(buf, T, Qb, m, n, nb, ib, "greedy")
+    Q = tq.from_tiled(Qb, m, m, nb)
+    assert (torch.linalg.norm(A - Q @ R) / torch.linalg.norm(A)).item() <= TOL_QR
+    assert torch.linalg.norm(torch.eye(n, dtype=torch.float64, device=DEV) - Q.T @ Q).item() <= TOL_QR
+    Rl = np.linalg.qr(A.cpu().numpy(), mode="r")
+    assert rel(nu.sign_normalise(R.cpu().numpy()), nu.sign_normalise(Rl)) <= TOL_R
+
+
+def test_config3_tall_full_size_gram():
+    """configs[3] as `bench.py --workload tall` runs it on one GPU: 524288 x 4096
+    (p = 2048, q = 16, nb = 256), Greedy. The oracle cannot run at this size, so
+    check properties that hold at any size: R^T R = A^T A (A = QR with Q
+    orthonormal), and R equals the Cholesky factor of A^T A up to row signs."""
+    p, q, nb, ib = 2048, 16, 256, 32
+    m, n = p * nb, q * nb
+    g = torch.Generator(device=DEV).manual_seed(5)
+    A = torch.randn(m * n, dtype=torch.float64, device=DEV, generator=g)      # tiled buffer, i.i.d. N(0,1)
+    Ad = tq.from_tiled(A, m, n, nb)
+    G = Ad.T @ Ad
+    del Ad
+    tq.tiled_qr(A, m, n, nb, ib, "greedy")
+    R = torch.triu(tq.from_tiled(A, m, n, nb)[:n])
+    err = (torch.linalg.norm(R.T @ R - G) / torch.linalg.norm(G)).item()
+    assert err <= 1e-13, err
+    # R equals the Cholesky factor of A^T A up to row signs
+    Lc = torch.linalg.cholesky(G)
+    assert rel(nu.sign_normalise(R.cpu().numpy()), Lc.T.cpu().numpy()) <= TOL_R
