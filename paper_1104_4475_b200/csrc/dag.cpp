@@ -282,12 +282,12 @@ void build_apply_graph(const std::vector<TileTask> &tt, int p, int qc, int nb, i
 // B200 kernels on nb = 200 tiles, from the per-task tracer; only the ratios matter).
 static double est_duration(int kind) {
   switch (kind) {
-    case K_GEQRT_B: case K_TTQRT_B: return 80;
-    case K_TSQRT_B: return 90;
+    case K_GEQRT_B: case K_TTQRT_B: return 71;
+    case K_TSQRT_B: return 80;
     case K_GEQRT_U: case K_TTQRT_U: case K_TSQRT_U: return 10;
-    case K_UNMQR: case K_AP_UNMQR: return 41;
-    case K_TTMQR: case K_AP_TTMQR: return 48;
-    case K_TSMQR: case K_AP_TSMQR: return 60;
+    case K_UNMQR: case K_AP_UNMQR: return 40;
+    case K_TTMQR: case K_AP_TTMQR: return 52;
+    case K_TSMQR: case K_AP_TSMQR: return 64;
     case K_GEQRT: return 450;
     case K_TTQRT: return 430;
     case K_TSQRT: return 500;
@@ -295,7 +295,7 @@ static double est_duration(int kind) {
   }
 }
 
-void finalize_dataflow(DevGraph &g, bool lookahead) {
+void finalize_dataflow(DevGraph &g, bool lookahead, int levels) {
   const int n = (int)g.tasks.size();
   std::vector<int32_t> cnt(n + 1, 0);
   for (int t = 0; t < n; ++t)
@@ -324,7 +324,8 @@ void finalize_dataflow(DevGraph &g, bool lookahead) {
   for (int t = 0; t < n; ++t) {
     DevTask &x = g.tasks[t];
     const int indeg = x.dep_end - x.dep_begin;
-    int level = lookahead ? std::min(kLevels - 1, (int)(kLevels * bl[t] / blmax)) : 0;
+    const int nlev = std::min(kLevels, std::max(1, levels));
+    int level = lookahead ? std::min(nlev - 1, (int)(nlev * bl[t] / blmax)) : 0;
     x.meta = indeg | (level << 16) | (chained[t] ? 1 << 20 : 0);
     x.dep_begin = cnt[t];
     x.dep_end = cnt[t + 1];

@@ -64,12 +64,12 @@ struct DevGraph {
 };
 
 // Convert the predecessor lists into successor lists, indegrees and the
-// priority level of every task (meta bits 16-19, kLevels levels from the
+// priority level of every task (meta bits 16-19, up to kLevels levels from the
 // task's estimated bottom level: longest path to the end of the graph);
 // chain targets get meta bit 20 (one virtual extra dependency held by the
 // chain owner). prioritize = false puts every task on level 0 (FIFO).
-constexpr int kLevels = 8;
-void finalize_dataflow(DevGraph &g, bool prioritize = true);
+constexpr int kLevels = 16;
+void finalize_dataflow(DevGraph &g, bool prioritize = true, int levels = kLevels);
 
 // Strip-refined factorization graph: every update task is split into
 // ceil(nb/ws) column strips of width ws; with split_panels (requires ws == ib)
