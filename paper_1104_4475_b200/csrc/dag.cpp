@@ -16,6 +16,7 @@
 // tile are disjoint).
 #include <algorithm>
 #include <numeric>
+#include <queue>
 #include "plan.h"
 
 namespace tqr {
@@ -295,7 +296,47 @@ static double est_duration(int kind) {
   }
 }
 
-void finalize_dataflow(DevGraph &g, bool lookahead, int levels) {
+// Non-preemptive list scheduling on nproc identical processors: whenever a
+// processor is free, start the ready task with the highest key. Returns the
+// makespan; start[t] receives each task's start time.
+static double list_schedule(const DevGraph &g, const std::vector<int32_t> &cnt, const std::vector<double> &key,
+                            int nproc, std::vector<double> &start) {
+  const int n = (int)g.tasks.size();
+  std::vector<int> indeg(n, 0);
+  for (int t = 0; t < n; ++t)
+    for (int x = cnt[t]; x < cnt[t + 1]; ++x) ++indeg[g.succ[x]];
+  using RT = std::pair<double, int>;                         // (key, task): max-heap of ready tasks
+  std::priority_queue<RT> ready;
+  using EV = std::pair<double, int>;                         // (finish time, task): min-heap of running
+  std::priority_queue<EV, std::vector<EV>, std::greater<EV>> running;
+  for (int t = 0; t < n; ++t)
+    if (indeg[t] == 0) ready.emplace(key[t], t);
+  double now = 0.0, mk = 0.0;
+  int free = nproc;
+  while (!ready.empty() || !running.empty()) {
+    while (free > 0 && !ready.empty()) {
+      const int t = ready.top().second;
+      ready.pop();
+      start[t] = now;
+      running.emplace(now + est_duration(g.tasks[t].kind), t);
+      --free;
+    }
+    if (running.empty()) break;
+    const double tf = running.top().first;
+    now = tf;
+    while (!running.empty() && running.top().first <= tf) {
+      const int t = running.top().second;
+      running.pop();
+      ++free;
+      mk = std::max(mk, tf);
+      for (int x = cnt[t]; x < cnt[t + 1]; ++x)
+        if (--indeg[g.succ[x]] == 0) ready.emplace(key[g.succ[x]], g.succ[x]);
+    }
+  }
+  return mk;
+}
+
+void finalize_dataflow(DevGraph &g, bool lookahead, int levels, int prio_rule, int nproc) {
   const int n = (int)g.tasks.size();
   std::vector<int32_t> cnt(n + 1, 0);
   for (int t = 0; t < n; ++t)
@@ -321,11 +362,43 @@ void finalize_dataflow(DevGraph &g, bool lookahead, int levels) {
     bl[t] = est_duration(g.tasks[t].kind) + m;
     blmax = std::max(blmax, bl[t]);
   }
+  // ASAP start of every task with the same estimates (tasks are in topological order)
+  std::vector<double> asap(n, 0.0);
+  for (int t = 0; t < n; ++t) {
+    const double f = asap[t] + est_duration(g.tasks[t].kind);
+    for (int x = cnt[t]; x < cnt[t + 1]; ++x) asap[g.succ[x]] = std::max(asap[g.succ[x]], f);
+  }
+  // priority key: 0 = bottom level; 1 = earliest ASAP start first; 2 = bottom level
+  // plus (CP - ASAP start): also lifts early tasks whose long chains have slack in the
+  // unbounded model but become critical once resources are limited
+  std::vector<double> key(n);
+  double kmax = 1e-9;
+  auto make_key = [&](int rule, double alpha, std::vector<double> &k) {
+    for (int t = 0; t < n; ++t)
+      k[t] = rule == 1 ? blmax - asap[t] : (rule == 2 ? bl[t] + alpha * (blmax - asap[t]) : bl[t]);
+  };
+  if (prio_rule == 3) {
+    // list-schedule the graph on `nproc` SMs with each candidate key (host DES with the
+    // duration estimates); keep the best and use its simulated start order as priority
+    std::vector<double> cand(n), best_start, start(n);
+    double best = 1e300;
+    for (double alpha : {0.0, 0.25, 0.5, 1.0, 2.0}) {
+      make_key(alpha == 0.0 ? 0 : 2, alpha, cand);
+      const double mk = list_schedule(g, cnt, cand, nproc, start);
+      if (mk < best) { best = mk; best_start = start; }
+    }
+    double smax = 1e-9;
+    for (int t = 0; t < n; ++t) smax = std::max(smax, best_start[t]);
+    for (int t = 0; t < n; ++t) key[t] = smax - best_start[t];       // earlier simulated start = higher
+  } else {
+    make_key(prio_rule, 1.0, key);
+  }
+  for (int t = 0; t < n; ++t) kmax = std::max(kmax, key[t]);
   for (int t = 0; t < n; ++t) {
     DevTask &x = g.tasks[t];
     const int indeg = x.dep_end - x.dep_begin;
     const int nlev = std::min(kLevels, std::max(1, levels));
-    int level = lookahead ? std::min(nlev - 1, (int)(nlev * bl[t] / blmax)) : 0;
+    int level = lookahead ? std::min(nlev - 1, std::max(0, (int)(nlev * key[t] / kmax))) : 0;
     x.meta = indeg | (level << 16) | (chained[t] ? 1 << 20 : 0);
     x.dep_begin = cnt[t];
     x.dep_end = cnt[t + 1];

@@ -69,7 +69,8 @@ struct DevGraph {
 // chain targets get meta bit 20 (one virtual extra dependency held by the
 // chain owner). prioritize = false puts every task on level 0 (FIFO).
 constexpr int kLevels = 16;
-void finalize_dataflow(DevGraph &g, bool prioritize = true, int levels = kLevels);
+void finalize_dataflow(DevGraph &g, bool prioritize = true, int levels = kLevels, int prio_rule = 0,
+                       int nproc = 148);
 
 // Strip-refined factorization graph: every update task is split into
 // ceil(nb/ws) column strips of width ws; with split_panels (requires ws == ib)

@@ -157,7 +157,7 @@ static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, in
   int ws = pick_ws(nb, ib);
   PlanKey key{dev, mode, p, q, qc, nb, ib, tree, bs, family,
               (ws * 4 + (env_int("TQR_SPLIT", 1) != 0) * 2 + (env_int("TQR_LOOKAHEAD", 1) != 0)) * 64 +
-                  env_int("TQR_LEVELS", kLevels)};
+                  env_int("TQR_LEVELS", kLevels) + 4096 * env_int("TQR_PRIO", 0)};
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_plans.find(key);
   if (it != g_plans.end()) { *out = it->second.get(); return 0; }
@@ -170,7 +170,10 @@ static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, in
   const bool split = env_int("TQR_SPLIT", 1) != 0 && ws == ib && nb > ib;
   if (mode == 0) build_factor_graph(tt, st, p, q, nb, ws, split, g);
   else build_apply_graph(tt, p, qc, nb, ws, mode == 1, g);
-  finalize_dataflow(g, env_int("TQR_LOOKAHEAD", 1) != 0, env_int("TQR_LEVELS", kLevels));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  finalize_dataflow(g, env_int("TQR_LOOKAHEAD", 1) != 0, env_int("TQR_LEVELS", kLevels), env_int("TQR_PRIO", 0),
+                    sms);
   auto pl = std::make_unique<DevPlan>();
   rc = upload(g, ws, *pl);
   if (rc < 0) return rc;

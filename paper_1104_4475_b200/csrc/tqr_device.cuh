@@ -24,7 +24,7 @@ constexpr int kTraceWords = 12;             // per-task trace record (diagnostic
 // scheduler control words (ints; each on its own 128-byte line): per priority
 // level l a queue head at kCtrlHead + 64 l and tail at kCtrlTail + 64 l
 constexpr int kCtrlHead = 0, kCtrlTail = 32, kCtrlDone = 64 * kLevels, kCtrlExit = 64 * kLevels + 32,
-              kCtrlWords = 64 * kLevels + 64;                    // ld of the 32 x 32 smem T / top / G blocks
+              kCtrlAvail = 64 * kLevels + 64, kCtrlWords = 64 * kLevels + 96;                    // ld of the 32 x 32 smem T / top / G blocks
 constexpr int kPanelScratch = 2 * 32 * kTld + 2 * 256 + 8 + 32;
 
 struct RunArgs {
@@ -535,21 +535,26 @@ __device__ __forceinline__ void larfg_scalars(double alpha, double xn2, double &
 // Ts must hold tau on the diagonal and zeros elsewhere on entry; X is scratch.
 __device__ void t_doubling(double *Ts, const double *G, double *X) {
   const int tid = threadIdx.x;
-  for (int sz = 1; sz < 32; sz <<= 1) {
-    const int per = sz * sz, n = (16 / sz) * per;      // entries per merge, total (= 16*sz <= 256)
-    if (tid < n) {                                       // X = G12 T22
-      const int u = tid / per, e = tid % per, i = e % sz, j = e / sz;
-      const int b0 = 2 * sz * u, b1 = b0 + sz;
+#pragma unroll
+  for (int lg = 0; lg < 5; ++lg) {                     // merge size sz = 2^lg
+    const int sz = 1 << lg;
+    const int u = tid >> (2 * lg), e = tid & (sz * sz - 1);
+    const int i = e & (sz - 1), j = e >> lg;
+    const int b0 = 2 * sz * u, b1 = b0 + sz;
+    const bool act = tid < 16 * sz;                    // (16/sz) merges of sz*sz entries
+    if (act) {                                         // X = G12 T22
       double acc = 0.0;
-      for (int m = 0; m <= j; ++m) acc = fma(G[(b0 + i) + (b1 + m) * kTld], Ts[(b1 + m) + (b1 + j) * kTld], acc);
+#pragma unroll
+      for (int m = 0; m < sz; ++m)
+        if (m <= j) acc = fma(G[(b0 + i) + (b1 + m) * kTld], Ts[(b1 + m) + (b1 + j) * kTld], acc);
       X[(b0 + i) + (b1 + j) * kTld] = acc;
     }
     __syncthreads();
-    if (tid < n) {                                       // T12 = -T11 X
-      const int u = tid / per, e = tid % per, i = e % sz, j = e / sz;
-      const int b0 = 2 * sz * u, b1 = b0 + sz;
+    if (act) {                                         // T12 = -T11 X
       double acc = 0.0;
-      for (int m = i; m < sz; ++m) acc = fma(Ts[(b0 + i) + (b0 + m) * kTld], X[(b0 + m) + (b1 + j) * kTld], acc);
+#pragma unroll
+      for (int m = 0; m < sz; ++m)
+        if (m >= i) acc = fma(Ts[(b0 + i) + (b0 + m) * kTld], X[(b0 + m) + (b1 + j) * kTld], acc);
       Ts[(b0 + i) + (b1 + j) * kTld] = -acc;
     }
     __syncthreads();
@@ -980,6 +985,8 @@ __device__ __forceinline__ void push_ready(const RunArgs &a, int t) {   // (chai
   const int q = (a.tasks[t].meta >> 16) & 15;
   const int pos = atomicAdd(&a.ctrl[kCtrlTail + 64 * q], 1);
   st_release64(a.queue + (size_t)q * a.ntask + pos, ((unsigned long long)(unsigned)a.epoch << 32) | (unsigned)t);
+  atomicAdd(&a.ctrl[kCtrlAvail], 1);   // idle CTAs poll this one word instead of every queue
+  if (a.trace) a.trace[kTraceWords * (size_t)t + 11] = globaltimer();   // diagnostics: push time
 }
 
 // claim the next slot of queue q if one is published; returns the task or -1
@@ -1029,11 +1036,15 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
       int t = s_chain;
       if (t < 0) {
         s_resident = 0;
+        unsigned backoff = 32;
         for (;;) {
+          if (ld_relaxed(&a.ctrl[kCtrlAvail]) > 0) {
+            for (int q = kLevels - 1; q >= 0 && t < 0; --q) t = try_pop(a, q);
+            if (t >= 0) { atomicSub(&a.ctrl[kCtrlAvail], 1); break; }
+          }
           if (ld_relaxed(&a.ctrl[kCtrlDone]) >= a.ntask) { t = -1; break; }
-          for (int q = kLevels - 1; q >= 0 && t < 0; --q) t = try_pop(a, q);
-          if (t >= 0) break;
-          __nanosleep(64);
+          __nanosleep(backoff);
+          backoff = backoff < 1024 ? backoff * 2 : 1024;
         }
       }
       s_task = t;
@@ -1063,7 +1074,7 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
         unsigned long long *tr = a.trace + kTraceWords * (size_t)t;
         tr[2] = globaltimer();
         tr[3] = ((unsigned long long)smid() << 32) | (unsigned)tk.kind;
-        for (int x = 0; x < 8; ++x) tr[4 + x] = s_prof[x];
+        for (int x = 0; x < 7; ++x) tr[4 + x] = s_prof[x];   // word 11 = push time
       }
       atomicAdd(&a.ctrl[kCtrlDone], 1);
       // panel chain: run the chained successor here if its other inputs are (or
@@ -1084,7 +1095,7 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
     const int n = atomicAdd(&a.ctrl[kCtrlExit], 1);
     if (n == a.nctas - 1) {
       for (int q = 0; q < kLevels; ++q) a.ctrl[kCtrlHead + 64 * q] = a.ctrl[kCtrlTail + 64 * q] = 0;
-      a.ctrl[kCtrlDone] = 0; a.ctrl[kCtrlExit] = 0;
+      a.ctrl[kCtrlDone] = 0; a.ctrl[kCtrlExit] = 0; a.ctrl[kCtrlAvail] = 0;
       __threadfence();
     }
   }

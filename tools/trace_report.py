@@ -111,3 +111,44 @@ for b in range(nb_):
     ov = np.clip(np.minimum(rd, hi) - np.maximum(rs, lo), 0, None)
     cpb.append((ov * panel).sum() / (hi - lo))
 print("  concurrent panel tasks per 5%:   " + " ".join(f"{u:4.1f}" for u in cpb))
+# executed critical chain: from the last task back through the predecessor that finished last;
+# split into execution time and queueing delay (inputs ready -> task started)
+preds = [[] for _ in range(len(tr))]
+for u in range(len(tr)):
+    for x in range(ptr[u], ptr[u + 1]):
+        preds[idx[x]].append(u)
+t = int(np.argmax(tr["done"]))
+exe = que = 0.0
+nchain = 0
+kinds_e, kinds_q = {}, {}
+while True:
+    nchain += 1
+    k = tq.KIND_NAMES[tr["kind"][t]]
+    d = (tr["done"][t] - tr["ready"][t]) / 1e3
+    exe += d
+    kinds_e[k] = kinds_e.get(k, 0) + d
+    if not preds[t]:
+        que += (tr["ready"][t] - t0) / 1e3
+        break
+    u = max(preds[t], key=lambda z: tr["done"][z])
+    q_ = max(0.0, (tr["ready"][t] - tr["done"][u]) / 1e3)
+    que += q_
+    kinds_q[k] = kinds_q.get(k, 0) + q_
+    t = u
+print(f"  executed chain: {nchain} tasks, execution {exe / 1e3:.3f} ms + queueing {que / 1e3:.3f} ms")
+print("   exec by kind (ms): " + ", ".join(f"{k} {v / 1e3:.2f}" for k, v in sorted(kinds_e.items(), key=lambda x: -x[1])))
+print("   queue by kind (ms): " + ", ".join(f"{k} {v / 1e3:.2f}" for k, v in sorted(kinds_q.items(), key=lambda x: -x[1])))
+if len(a) > 6 and a[6] == "chain":
+    t = int(np.argmax(tr["done"]))
+    rows = []
+    while True:
+        rows.append(t)
+        if not preds[t]:
+            break
+        t = max(preds[t], key=lambda z: tr["done"][z])
+    for t in reversed(rows):
+        u = max(preds[t], key=lambda z: tr["done"][z]) if preds[t] else None
+        rdy = (tr["done"][u] - t0) / 1e3 if u is not None else 0.0
+        pushed = (tr["c_store"][t] - t0) / 1e3 if tr["c_store"][t] > 0 else float("nan")
+        print(f"   {tq.KIND_NAMES[tr['kind'][t]]:8s} i={tr['i'][t]:2d} piv={tr['piv'][t]:2d} k={tr['k'][t]} j={tr['j'][t]} s={tr['s'][t]} "
+              f"inputs {rdy:8.1f} pushed {pushed:8.1f} start {(tr['ready'][t] - t0) / 1e3:8.1f} done {(tr['done'][t] - t0) / 1e3:8.1f} us")
