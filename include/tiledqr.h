@@ -162,6 +162,14 @@ int64_t tqr_trace_fetch(uint64_t *out, int64_t cap);
  * succ_ptr[ntask+1], succ[...]. Returns the number of edges or TQR_E*. */
 int64_t tqr_trace_graph(int32_t *succ_ptr, int32_t *succ, int64_t cap);
 
+/* Diagnostics, host only (no GPU): the device task graph tiled_qr would run
+ * (strip width ws, 0 = default; split = per-inner-block panel tasks). Fills
+ * out_tasks with 8 int32 per task (kind, i, piv, k, j, s, chain, meta) in
+ * priority order and the successor CSR (succ_ptr[ntask+1], succ). With null
+ * outputs it only returns the task count. Returns ntask or a TQR_E* code. */
+int64_t tqr_plan_graph(int m, int n, int nb, int ib, int tree, int bs, int family, int ws, int split,
+                       int32_t *out_tasks, int64_t task_cap, int32_t *succ_ptr, int32_t *succ, int64_t succ_cap);
+
 /* Number of kernel launches the last device call issued (for bench accounting). */
 int tqr_last_launch_count(void);
 

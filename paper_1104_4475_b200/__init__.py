@@ -41,6 +41,7 @@ _SIGS = {
     "tqr_trace_enable": (ctypes.c_int, [ctypes.c_int]),
     "tqr_trace_fetch": (ctypes.c_int64, [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int64]),
     "tqr_trace_graph": (ctypes.c_int64, [_I32P, _I32P, ctypes.c_int64]),
+    "tqr_plan_graph": (ctypes.c_int64, [ctypes.c_int] * 9 + [_I32P, ctypes.c_int64, _I32P, _I32P, ctypes.c_int64]),
     "tqr_last_launch_count": (ctypes.c_int, []),
     "tqr_release_plans": (None, []),
     "tqr_last_error": (ctypes.c_char_p, []),
@@ -215,6 +216,19 @@ def trace_graph(ntask: int):
     idx = np.zeros(cap, np.int32)
     n = _check(lib().tqr_trace_graph(_ptr(ptr), _ptr(idx), cap))
     return ptr[: ntask + 1].copy(), idx[:n].copy()
+
+
+def plan_graph(m: int, n: int, nb: int, ib: int = 32, tree="greedy", bs: int = 1, family="TT", ws: int = 0,
+               split: bool = True):
+    """Host-only diagnostic: the device task graph (tasks[ntask, 8], succ_ptr, succ)."""
+    args = (m, n, nb, ib, _tree(tree), bs, _fam(family), ws, 1 if split else 0)
+    nt = _check(lib().tqr_plan_graph(*args, None, 0, None, None, 0))
+    tasks = np.zeros(8 * nt, np.int32)
+    ptr = np.zeros(nt + 1, np.int32)
+    cap = 16 * nt + 16
+    succ = np.zeros(cap, np.int32)
+    _check(lib().tqr_plan_graph(*args, _ptr(tasks), tasks.size, _ptr(ptr), _ptr(succ), cap))
+    return tasks.reshape(nt, 8), ptr, succ[: ptr[-1]].copy()
 
 
 def last_launch_count() -> int:

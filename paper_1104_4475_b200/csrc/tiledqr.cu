@@ -105,6 +105,8 @@ static int pick_ws(int nb, int ib) {
   return 8;
 }
 
+static int check_shape(int m, int n, int nb, int ib, int &p, int &q);
+
 // ---- plan cache -------------------------------------------------------------
 struct DevPlan {
   DevTask *tasks = nullptr;
@@ -180,6 +182,38 @@ static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, in
   *out = pl.get();
   g_plans[key] = std::move(pl);
   return 0;
+}
+
+// Host-only view of the device task graph (no GPU needed): the same builder
+// get_plan uses. out_tasks: 8 int32 per task (kind, i, piv, k, j, s, chain,
+// meta); succ_ptr[ntask+1], succ[...]. Returns ntask or TQR_E*.
+extern "C" int64_t tqr_plan_graph(int m, int n, int nb, int ib, int tree, int bs, int family, int ws, int split,
+                                  int32_t *out_tasks, int64_t task_cap, int32_t *succ_ptr, int32_t *succ,
+                                  int64_t succ_cap) {
+  int p, q;
+  int rc = check_shape(m, n, nb, ib, p, q);
+  if (rc < 0) return rc;
+  if (ws <= 0) ws = pick_ws(nb, ib);
+  std::vector<TileTask> tt;
+  std::vector<int64_t> st, fin;
+  int64_t mk;
+  rc = tile_sim(p, q, tree, bs, family, tt, st, fin, mk);
+  if (rc < 0) return rc;
+  DevGraph g;
+  build_factor_graph(tt, st, p, q, nb, ws, split != 0 && ws == ib && nb > ib, g);
+  finalize_dataflow(g, true, kLevels, 0, 148);
+  const int64_t nt = (int64_t)g.tasks.size();
+  if (!out_tasks || !succ_ptr || !succ) return nt;          // size query
+  if (task_cap < 8 * nt || succ_cap < (int64_t)g.succ.size()) return fail(TQR_ECAP, "tqr_plan_graph: capacity");
+  for (int64_t t = 0; t < nt; ++t) {
+    const DevTask &d = g.tasks[t];
+    int32_t *o = out_tasks + 8 * t;
+    o[0] = d.kind; o[1] = d.i; o[2] = d.piv; o[3] = d.k; o[4] = d.j; o[5] = d.s; o[6] = d.chain; o[7] = d.meta;
+    succ_ptr[t] = d.dep_begin;
+  }
+  succ_ptr[nt] = (int32_t)g.succ.size();
+  std::copy(g.succ.begin(), g.succ.end(), succ);
+  return nt;
 }
 
 extern "C" void tqr_release_plans(void) {
