@@ -219,22 +219,34 @@ def run_gpu(args, rank, world, local_rank):
     total_flops = FLOPS * len(TREES) * args.steps * world
     value = total_flops / (max_ms / 1e3) / 1e9
 
-    # end to end through the public API on host buffers (pinned): H2D of A, factor, D2H of A and T
+    # end to end through the public API on host buffers (pinned): every factorization
+    # uploads A, factors, and downloads A (R and V) and T; tiled_qr_host_async pipelines
+    # the copies of consecutive calls with the neighbouring factorizations
     pin_A = torch.empty(M * N, dtype=torch.float64, pin_memory=True)
-    pin_T = torch.empty(tq.t_size(M, N, NB, IB), dtype=torch.float64, pin_memory=True)
-    e2e_ms = 0.0
+    pin_A.numpy()[:] = A_host
+    outs = [(torch.empty(M * N, dtype=torch.float64, pin_memory=True),
+             torch.empty(tq.t_size(M, N, NB, IB), dtype=torch.float64, pin_memory=True)) for _ in range(2)]
     e2e_steps = max(1, min(args.steps, 3))
-    for it in range(e2e_steps + 1):
-        for (tree, bs) in TREES:
-            pin_A.numpy()[:] = A_host
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            tq.tiled_qr_host(pin_A.numpy(), M, N, NB, IB, tree, bs, "TT", T_host=pin_T.numpy(), stream=stream)
-            e1.record(stream)
-            e1.synchronize()
-            if it > 0:
-                e2e_ms += e0.elapsed_time(e1)
+
+    def e2e_run(nsteps):
+        c = 0
+        for _ in range(nsteps):
+            for (tree, bs) in TREES:
+                R_o, T_o = outs[c & 1]
+                tq.tiled_qr_host_async(pin_A.numpy(), R_o.numpy(), T_o.numpy(), M, N, NB, IB, tree, bs, "TT",
+                                       stream=stream)
+                c += 1
+        tq.host_wait()
+
+    e2e_run(1)                                             # warm-up (plans, scratch)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    e2e_run(e2e_steps)
+    e1.record(stream)
+    e1.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
     t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -264,7 +276,8 @@ def run_gpu(args, rank, world, local_rank):
                      "flops_per_launch": FLOPS, "avg_launch_ms": avg_launch_ms},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "tiled_qr_host (pinned host buffers; H2D A, factor, D2H A and T, stream sync)"},
+                "api": "tiled_qr_host_async (pinned host buffers; per factorization H2D A, factor, D2H A and T; "
+                       "copies pipelined with neighbouring factorizations; CUDA events incl. the final wait)"},
         "gpu_launches": launches_per * len(TREES) * args.steps,
     }
     if not args.no_cpu_baseline and world == 1:

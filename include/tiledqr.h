@@ -170,6 +170,17 @@ int64_t tqr_trace_graph(int32_t *succ_ptr, int32_t *succ, int64_t cap);
 int64_t tqr_plan_graph(int m, int n, int nb, int ib, int tree, int bs, int family, int ws, int split,
                        int32_t *out_tasks, int64_t task_cap, int32_t *succ_ptr, int32_t *succ, int64_t succ_cap);
 
+/* tiled_qr_host_async — pipelined end-to-end variant: enqueues the upload of
+ * A_host (pinned host memory for real overlap), the factorization on
+ * `stream`, and the download of the factored A (R and V) into R_host and of T
+ * into T_host, and returns. Consecutive calls alternate between two device
+ * slots and two internal copy streams, so copies overlap the neighbouring
+ * calls' compute. A_host must stay valid and R_host/T_host must not be read
+ * until tqr_host_wait() returns. Returns 0 or a negative TQR_E* code. */
+int tiled_qr_host_async(int m, int n, int nb, int ib, int tree, int bs, int family,
+                        const double *A_host, double *R_host, double *T_host, void *stream);
+int tqr_host_wait(void);
+
 /* Number of kernel launches the last device call issued (for bench accounting). */
 int tqr_last_launch_count(void);
 

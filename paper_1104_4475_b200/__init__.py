@@ -18,7 +18,7 @@ import numpy as np
 
 __all__ = [
     "TREES", "FAMILIES", "lib", "elim_list", "critical_path", "tiled_times", "tiled_qr",
-    "apply_qt", "apply_q", "tiled_qr_host", "to_tiled", "from_tiled", "t_size", "last_launch_count",
+    "apply_qt", "apply_q", "tiled_qr_host", "tiled_qr_host_async", "host_wait", "to_tiled", "from_tiled", "t_size", "last_launch_count",
 ]
 
 TREES = {"flat": 0, "fibonacci": 1, "greedy": 2, "binary": 3, "plasma": 4, "merge": 5}
@@ -42,6 +42,8 @@ _SIGS = {
     "tqr_trace_fetch": (ctypes.c_int64, [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int64]),
     "tqr_trace_graph": (ctypes.c_int64, [_I32P, _I32P, ctypes.c_int64]),
     "tqr_plan_graph": (ctypes.c_int64, [ctypes.c_int] * 9 + [_I32P, ctypes.c_int64, _I32P, _I32P, ctypes.c_int64]),
+    "tiled_qr_host_async": (ctypes.c_int, [ctypes.c_int] * 7 + [_VP, _VP, _VP, _VP]),
+    "tqr_host_wait": (ctypes.c_int, []),
     "tqr_last_launch_count": (ctypes.c_int, []),
     "tqr_release_plans": (None, []),
     "tqr_last_error": (ctypes.c_char_p, []),
@@ -229,6 +231,20 @@ def plan_graph(m: int, n: int, nb: int, ib: int = 32, tree="greedy", bs: int = 1
     succ = np.zeros(cap, np.int32)
     _check(lib().tqr_plan_graph(*args, _ptr(tasks), tasks.size, _ptr(ptr), _ptr(succ), cap))
     return tasks.reshape(nt, 8), ptr, succ[: ptr[-1]].copy()
+
+
+def tiled_qr_host_async(A_host: np.ndarray, R_host: np.ndarray, T_host: np.ndarray, m: int, n: int, nb: int,
+                        ib: int = 32, tree="greedy", bs: int = 1, family="TT", stream=None):
+    """Pipelined end-to-end call (pinned host buffers): upload, factor, download, no wait."""
+    for b in (A_host, R_host, T_host):
+        assert b.dtype == np.float64 and b.flags.c_contiguous
+    s = _stream(stream) if stream is not None else ctypes.c_void_p(0)
+    _check(lib().tiled_qr_host_async(m, n, nb, ib, _tree(tree), bs, _fam(family), ctypes.c_void_p(A_host.ctypes.data),
+                                     ctypes.c_void_p(R_host.ctypes.data), ctypes.c_void_p(T_host.ctypes.data), s))
+
+
+def host_wait():
+    _check(lib().tqr_host_wait())
 
 
 def last_launch_count() -> int:

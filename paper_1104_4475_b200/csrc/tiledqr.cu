@@ -377,3 +377,81 @@ extern "C" int tiled_qr_host(int m, int n, int nb, int ib, int tree, int bs, int
   CUDA_TRY(cudaStreamSynchronize(s));
   return 0;
 }
+
+// ---- pipelined end-to-end calls (two device slots, dedicated copy streams) ----
+// Call k uses slot k % 2: H2D on the upload stream (after the slot's previous
+// download finished), the factorization on the caller's stream (after the
+// upload), the download of A and T on the download stream (after the
+// factorization). Consecutive calls therefore overlap their copies with the
+// neighbours' compute. tqr_host_wait() waits for everything issued.
+struct AsyncPipe {
+  int dev = -1;
+  size_t na = 0, nt = 0;
+  double *A[2] = {nullptr, nullptr}, *T[2] = {nullptr, nullptr};
+  cudaStream_t up = nullptr, down = nullptr;
+  cudaEvent_t uploaded[2], computed[2], downloaded[2];
+  unsigned long long calls = 0;
+};
+static std::mutex g_pmu;
+static AsyncPipe g_pipe;
+
+static int pipe_init(AsyncPipe &P, int dev, size_t na, size_t nt) {
+  if (P.dev == dev && P.na >= na && P.nt >= nt) return 0;
+  if (P.dev >= 0) {
+    cudaStreamSynchronize(P.down);
+    for (int k = 0; k < 2; ++k) { cudaFree(P.A[k]); cudaFree(P.T[k]); }
+  } else {
+    CUDA_TRY(cudaStreamCreateWithFlags(&P.up, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&P.down, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      CUDA_TRY(cudaEventCreateWithFlags(&P.uploaded[k], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&P.computed[k], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&P.downloaded[k], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventRecord(P.downloaded[k], P.down));
+    }
+  }
+  for (int k = 0; k < 2; ++k) {
+    CUDA_TRY(cudaMalloc(&P.A[k], na * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&P.T[k], nt * sizeof(double)));
+  }
+  P.dev = dev; P.na = na; P.nt = nt;
+  return 0;
+}
+
+extern "C" int tiled_qr_host_async(int m, int n, int nb, int ib, int tree, int bs, int family,
+                                   const double *A_host, double *R_host, double *T_host, void *stream) {
+  int p, q;
+  int rc = check_shape(m, n, nb, ib, p, q);
+  if (rc < 0) return rc;
+  if (!A_host || !R_host || !T_host) return fail(TQR_EINVAL, "tiled_qr_host_async: null pointer");
+  std::lock_guard<std::mutex> lk(g_pmu);
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  const size_t na = (size_t)m * n, nt = (size_t)p * q * 2 * ib * nb;
+  rc = pipe_init(g_pipe, dev, na, nt);
+  if (rc < 0) return rc;
+  AsyncPipe &P = g_pipe;
+  const int k = (int)(P.calls++ & 1);
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaStreamWaitEvent(P.up, P.downloaded[k], 0));
+  CUDA_TRY(cudaMemcpyAsync(P.A[k], A_host, na * sizeof(double), cudaMemcpyHostToDevice, P.up));
+  CUDA_TRY(cudaEventRecord(P.uploaded[k], P.up));
+  CUDA_TRY(cudaStreamWaitEvent(s, P.uploaded[k], 0));
+  rc = tiled_qr(m, n, nb, ib, tree, bs, family, P.A[k], P.T[k], stream);
+  if (rc < 0) return rc;
+  CUDA_TRY(cudaEventRecord(P.computed[k], s));
+  CUDA_TRY(cudaStreamWaitEvent(P.down, P.computed[k], 0));
+  CUDA_TRY(cudaMemcpyAsync(R_host, P.A[k], na * sizeof(double), cudaMemcpyDeviceToHost, P.down));
+  CUDA_TRY(cudaMemcpyAsync(T_host, P.T[k], nt * sizeof(double), cudaMemcpyDeviceToHost, P.down));
+  CUDA_TRY(cudaEventRecord(P.downloaded[k], P.down));
+  return 0;
+}
+
+extern "C" int tqr_host_wait(void) {
+  std::lock_guard<std::mutex> lk(g_pmu);
+  if (g_pipe.dev >= 0) {
+    CUDA_TRY(cudaStreamSynchronize(g_pipe.up));
+    CUDA_TRY(cudaStreamSynchronize(g_pipe.down));
+  }
+  return 0;
+}

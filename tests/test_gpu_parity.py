@@ -273,3 +273,22 @@ def test_config3_tall_full_size_gram():
     # R equals the Cholesky factor of A^T A up to row signs
     Lc = torch.linalg.cholesky(G)
     assert rel(nu.sign_normalise(R.cpu().numpy()), Lc.T.cpu().numpy()) <= TOL_R
+
+
+def test_host_async_pipeline():
+    """tiled_qr_host_async: several pipelined end-to-end calls on pinned host
+    buffers give the same factors as the device API (and as the oracle)."""
+    p, q, nb, ib = 6, 3, 64, 32
+    m, n = p * nb, q * nb
+    mats = [qrinputs.gaussian(m, n, 300 + s) for s in range(3)]
+    ins = [torch.from_numpy(qrinputs.to_tiles(Ad, nb)).pin_memory() for Ad in mats]
+    outs = [(torch.empty(m * n, dtype=torch.float64).pin_memory(),
+             torch.empty(tq.t_size(m, n, nb, ib), dtype=torch.float64).pin_memory()) for _ in mats]
+    for x, (R_o, T_o), tree in zip(ins, outs, ("greedy", "flat", "fibonacci")):
+        tq.tiled_qr_host_async(x.numpy(), R_o.numpy(), T_o.numpy(), m, n, nb, ib, tree)
+    tq.host_wait()
+    for Ad, (R_o, T_o), tree in zip(mats, outs, ("greedy", "flat", "fibonacci")):
+        F = nu.tiled_qr(Ad, nb, ib, schemes.elim_list(tree, p, q), "TT")
+        got = qrinputs.from_tiles(R_o.numpy(), p, q, nb)
+        assert rel(got, F.A) <= TOL_R
+        assert rel(T_o.numpy()[: F.T.size], F.T) <= TOL_R
