@@ -53,12 +53,16 @@ enum tqr_tree {
   TQR_BINARY = 3,     /* BinaryTree, lines 914-918 */
   TQR_PLASMA = 4,     /* PlasmaTree(BS): flat inside domains of BS rows + binary
                          merge of the domain heads, lines 936-953 */
-  TQR_MERGE = 5       /* merge of two stacked tile-upper-triangular R factors
+  TQR_MERGE = 5,      /* merge of two stacked tile-upper-triangular R factors
                          [R1; R2] (p = 2q): column k zeroes tiles (q+t, k),
                          t = 1..k, against pivot row k. Used by the cross-GPU
                          reduction of tall-skinny matrices: the
                          input's diagonal tiles count as triangles, tiles below
                          them as structural zeros (they must hold zeros). */
+  TQR_ASAP = 6,       /* ASAP, lines 666-682: eliminations decided during the
+                         tiled execution (start as soon as two rows are ready) */
+  TQR_GRASAP = 7      /* Grasap(k), lines 685-692: Greedy on columns 1..q-k,
+                         ASAP on the last k columns; k is passed as `bs` */
 };
 
 /* Kernel families, §2.1 (lines 231-352) */

@@ -12,6 +12,8 @@ Modules
             coarse-grain time-steps (Table 2)
   dag       kernel-task expansion (Algorithms 2-3), weighted discrete-event
             simulation (critical paths, Tables 3/6), closed forms (Thm 1, Props 1-2)
+  asap      the tiled ASAP / Grasap(k) algorithms (§3.2), decided by an
+            incremental discrete-event simulation
   numeric   fp64 tile kernels GEQRT/TSQRT/TTQRT/UNMQR/TSMQR/TTMQR written as
             textbook Householder reflections, the tiled QR driven by an
             elimination list, Q / Q^T application, and an independent

@@ -21,7 +21,7 @@ __all__ = [
     "apply_qt", "apply_q", "tiled_qr_host", "tiled_qr_host_async", "host_wait", "to_tiled", "from_tiled", "t_size", "last_launch_count",
 ]
 
-TREES = {"flat": 0, "fibonacci": 1, "greedy": 2, "binary": 3, "plasma": 4, "merge": 5}
+TREES = {"flat": 0, "fibonacci": 1, "greedy": 2, "binary": 3, "plasma": 4, "merge": 5, "asap": 6, "grasap": 7}
 FAMILIES = {"TT": 0, "TS": 1}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))

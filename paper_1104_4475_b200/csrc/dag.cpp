@@ -21,6 +21,89 @@
 
 namespace tqr {
 
+// ---- ASAP / Grasap(k) (§3.2) -----------------------
+// ASAP decides its eliminations during the tiled execution: at every instant,
+// in every column, with r rows ready (tile a triangle, not inside a running
+// TTQRT), s = r/2 eliminations start, the bottom s ready rows zeroed by the s
+// ready rows right above them. Grasap(k) runs Greedy's list on the first q-k
+// columns, then ASAP. The execution model is the TT expansion + unbounded
+// processors of expand/simulate, tracked incrementally here through the finish
+// time of every tile's last writer (reading R11).
+void grasap_elims(int p, int q, int k_asap, std::vector<Elim> &out) {
+  out.clear();
+  const int kmax = std::min(p, q);
+  std::vector<int64_t> lastfin((size_t)(p + 1) * (q + 1), 0);
+  std::vector<char> tri((size_t)(p + 1) * (q + 1), 0);
+  auto at = [q](int r, int c) { return (size_t)r * (q + 1) + c; };
+  auto emit = [&](int weight, int64_t readfin, int r1, int c1, int r2, int c2) {
+    int64_t st = std::max(readfin, lastfin[at(r1, c1)]);
+    if (r2 >= 0) st = std::max(st, lastfin[at(r2, c2)]);
+    const int64_t fin = st + weight;
+    lastfin[at(r1, c1)] = fin;
+    if (r2 >= 0) lastfin[at(r2, c2)] = fin;
+    return fin;
+  };
+  auto factor = [&](int r, int k) {
+    const int64_t g = emit(kind_weight(K_GEQRT), 0, r, k, -1, 0);
+    for (int j = k + 1; j <= q; ++j) emit(kind_weight(K_UNMQR), g, r, j, -1, 0);
+    tri[at(r, k)] = 1;
+    return g;
+  };
+  auto eliminate = [&](int i, int piv, int k) {
+    if (!tri[at(piv, k)]) factor(piv, k);
+    if (!tri[at(i, k)]) factor(i, k);
+    const int64_t x = emit(kind_weight(K_TTQRT), 0, piv, k, i, k);
+    for (int j = k + 1; j <= q; ++j) emit(kind_weight(K_TTMQR), x, piv, j, i, j);
+    out.push_back({i, piv, k, 0});
+    return x;
+  };
+  const int first = q - k_asap + 1;        // first ASAP column
+  if (first > 1) {
+    std::vector<Elim> gl;
+    std::string err;
+    build_elim_list(p, q, 2, 1, gl, err);
+    for (const Elim &e : gl)
+      if (e.k < first) eliminate(e.i, e.piv, e.k);
+  }
+  if (first > kmax) return;
+  // ready[k][r] = time row r is ready in column k (-1 = not ready / done)
+  std::vector<std::vector<int64_t>> ready(kmax + 2, std::vector<int64_t>(p + 1, -1));
+  std::vector<int> left(kmax + 2, 0);      // rows still to zero in each ASAP column
+  for (int k = first; k <= kmax; ++k) left[k] = p - k;
+  std::vector<char> zeroed_prev((size_t)p + 1, 0);
+  for (const Elim &e : out)
+    if (e.k == first - 1) zeroed_prev[e.i] = 1;
+  for (int r = first; r <= p; ++r)
+    if (first == 1 || zeroed_prev[r]) ready[first][r] = factor(r, first);
+  int64_t t = 0;
+  for (;;) {
+    // next instant with a ready row
+    int64_t tn = -1;
+    for (int k = first; k <= kmax; ++k)
+      for (int r = k; r <= p; ++r)
+        if (ready[k][r] >= t && (tn < 0 || ready[k][r] < tn)) tn = ready[k][r];
+    if (tn < 0) break;
+    t = tn;
+    for (int k = first; k <= kmax; ++k) {
+      if (left[k] == 0) continue;
+      std::vector<int> rows;
+      for (int r = k; r <= p; ++r)
+        if (ready[k][r] >= 0 && ready[k][r] <= t) rows.push_back(r);
+      const int nrow = (int)rows.size(), s = nrow / 2;
+      for (int x = 0; x < s; ++x) {
+        const int i = rows[nrow - s + x], pv = rows[nrow - 2 * s + x];
+        const int64_t done = eliminate(i, pv, k);
+        ready[k][i] = -1;
+        ready[k][pv] = done;
+        --left[k];
+        if (k + 1 <= kmax) ready[k + 1][i] = factor(i, k + 1);
+      }
+      if (left[k] == 0) std::fill(ready[k].begin(), ready[k].end(), -1);
+    }
+    ++t;      // every later event is at a strictly larger integer time
+  }
+}
+
 void expand(const std::vector<Elim> &lst, int p, int q, int family, std::vector<TileTask> &tasks,
             bool merge_input) {
   tasks.clear();

@@ -25,6 +25,10 @@ int kind_weight(int kind);   // Table 1 weights in units of nb^3/3
 // Elimination lists of every tree (trees.cpp). Returns false on bad args.
 bool build_elim_list(int p, int q, int tree, int bs, std::vector<Elim> &out, std::string &err);
 
+// ASAP (k_asap = q) / Grasap(k_asap) eliminations, decided by the tiled
+// discrete-event execution (dag.cpp).
+void grasap_elims(int p, int q, int k_asap, std::vector<Elim> &out);
+
 // Tile-level task of the expanded DAG (Algorithms 2-3); 1-based indices.
 struct TileTask {
   int kind, i, piv, k, j;          // j = updated column (updates only), else 0

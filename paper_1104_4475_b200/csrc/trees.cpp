@@ -147,6 +147,11 @@ bool build_elim_list(int p, int q, int tree, int bs, std::vector<Elim> &out, std
     case 5:
       if (p != 2 * q) { err = "elim_list: the merge scheme needs p = 2q"; return false; }
       merge(q, out); coarse_asap(p, out); break;
+    case 6:
+      grasap_elims(p, q, q, out); coarse_asap(p, out); break;
+    case 7:
+      if (bs < 0 || bs > q) { err = "elim_list: Grasap(k) needs 0 <= k <= q (passed as bs)"; return false; }
+      grasap_elims(p, q, bs, out); coarse_asap(p, out); break;
     default: err = "elim_list: unknown tree"; return false;
   }
   if (tree == 1 || tree == 2) {

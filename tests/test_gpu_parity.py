@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 import qrinputs
+from oracle import asap
 from oracle import numeric as nu
 from oracle import schemes
 
@@ -45,11 +46,19 @@ def gpu_Q(buf, T, m, n, nb, ib, tree, bs, family):
     return qrinputs.from_tiles(Cb.cpu().numpy(), m // nb, n // nb, nb)
 
 
+def oracle_list(tree, p, q, bs):
+    if tree == "asap":
+        return asap.grasap_list(p, q, q)[0]
+    if tree == "grasap":
+        return asap.grasap_list(p, q, bs)[0]
+    return schemes.elim_list(tree, p, q, bs)
+
+
 def compare_with_oracle(A, nb, ib, tree, bs, family, tol=TOL_R):
     m, n = A.shape
     p, q = m // nb, n // nb
     buf, T = run_gpu(A, nb, ib, tree, bs, family)
-    F = nu.tiled_qr(A, nb, ib, schemes.elim_list(tree, p, q, bs), family)
+    F = nu.tiled_qr(A, nb, ib, oracle_list(tree, p, q, bs), family)
     got = qrinputs.from_tiles(buf.cpu().numpy(), p, q, nb)
     # R (north_star: after row-sign normalisation)
     Rg = np.triu(got[:n, :n])
@@ -108,6 +117,15 @@ def test_config0_greedy_full_checks():
     # independent unblocked Householder QR (oracle) and LAPACK agree too
     Ru, _ = nu.householder_qr(A)
     assert rel(nu.sign_normalise(R), nu.sign_normalise(Ru)) <= TOL_R
+
+
+@pytest.mark.parametrize("tree,bs", [("asap", 0), ("grasap", 1)])
+def test_factor_parity_asap(tree, bs):
+    """The ASAP / Grasap(1) lists (decided by the tiled execution, §3.2) drive the
+    same kernels; parity with the oracle on the same lists."""
+    for (p, q, nb, ib) in [(8, 4, 32, 32), (6, 3, 20, 8), (4, 2, 72, 32), (3, 3, 64, 32)]:
+        A = qrinputs.gaussian(p * nb, q * nb, 4000 + p + q)
+        compare_with_oracle(A, nb, ib, tree, bs, "TT")
 
 
 @pytest.mark.parametrize("tree,bs,family", [("greedy", 1, "TT"), ("fibonacci", 1, "TS"), ("plasma", 3, "TT")])
