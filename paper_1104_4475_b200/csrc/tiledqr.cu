@@ -113,13 +113,14 @@ struct DevPlan {
   int32_t *succ = nullptr;
   int32_t *roots = nullptr;
   unsigned *cnt = nullptr;                // per-task arrivals (accumulate epoch x indegree)
-  unsigned long long *queue = nullptr;    // kLevels x ntask ready-queue slots (epoch-tagged)
+  unsigned long long *queue = nullptr;    // ntask ready-queue slots, split by level (epoch-tagged)
   int *ctrl = nullptr;                    // scheduler counters (kCtrlWords ints)
   unsigned long long *trace = nullptr;    // diagnostic per-task timestamps
   std::vector<DevTask> host_tasks;        // kept for tqr_trace_fetch
   int ntask = 0, nroots = 0;
   int epoch = 0;
   int ws = 0;
+  int qoff[kLevels + 1] = {0};            // per-level queue offsets
   ~DevPlan() {
     cudaFree(tasks); cudaFree(succ); cudaFree(roots); cudaFree(cnt); cudaFree(queue); cudaFree(ctrl);
     cudaFree(trace);
@@ -140,13 +141,16 @@ static int upload(const DevGraph &g, int ws, DevPlan &pl) {
   CUDA_TRY(cudaMalloc(&pl.succ, sizeof(int32_t) * (g.succ.empty() ? 1 : g.succ.size())));
   CUDA_TRY(cudaMalloc(&pl.roots, sizeof(int32_t) * (g.roots.empty() ? 1 : g.roots.size())));
   CUDA_TRY(cudaMalloc(&pl.cnt, sizeof(unsigned) * n1));
-  CUDA_TRY(cudaMalloc(&pl.queue, sizeof(unsigned long long) * kLevels * n1));
+  for (int l = 0; l <= kLevels; ++l) pl.qoff[l] = 0;
+  for (const DevTask &t : g.tasks) pl.qoff[((t.meta >> 16) & 15) + 1]++;
+  for (int l = 0; l < kLevels; ++l) pl.qoff[l + 1] += pl.qoff[l];
+  CUDA_TRY(cudaMalloc(&pl.queue, sizeof(unsigned long long) * n1));
   CUDA_TRY(cudaMalloc(&pl.ctrl, sizeof(int) * kCtrlWords));
   if (!g.tasks.empty()) CUDA_TRY(cudaMemcpy(pl.tasks, g.tasks.data(), sizeof(DevTask) * g.tasks.size(), cudaMemcpyHostToDevice));
   if (!g.succ.empty()) CUDA_TRY(cudaMemcpy(pl.succ, g.succ.data(), sizeof(int32_t) * g.succ.size(), cudaMemcpyHostToDevice));
   if (!g.roots.empty()) CUDA_TRY(cudaMemcpy(pl.roots, g.roots.data(), sizeof(int32_t) * g.roots.size(), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemset(pl.cnt, 0, sizeof(unsigned) * n1));
-  CUDA_TRY(cudaMemset(pl.queue, 0, sizeof(unsigned long long) * kLevels * n1));
+  CUDA_TRY(cudaMemset(pl.queue, 0, sizeof(unsigned long long) * n1));
   CUDA_TRY(cudaMemset(pl.ctrl, 0, sizeof(int) * kCtrlWords));
   return 0;
 }
@@ -288,6 +292,7 @@ static int launch(DevPlan *pl, int p, int q, int nb, int ib, double *A, double *
   RunArgs a;
   a.tasks = pl->tasks; a.succ = pl->succ; a.roots = pl->roots; a.nroots = pl->nroots; a.ntask = pl->ntask;
   a.cnt = pl->cnt; a.queue = pl->queue; a.ctrl = pl->ctrl; a.epoch = ++pl->epoch;
+  for (int l = 0; l <= kLevels; ++l) a.qoff[l] = pl->qoff[l];
   a.A = A; a.T = T; a.C = C;
   a.p = p; a.q = q; a.nb = nb; a.ib = ib; a.ws = pl->ws; a.trans = trans;
   a.tma = env_int("TQR_TMA", 0);   // 1-D TMA bulk path (measured ~4% slower than cp.async here)

@@ -34,7 +34,9 @@ struct RunArgs {
   int nroots;
   int ntask;
   unsigned *cnt;                // per-task arrivals, accumulated over launches (epoch * indegree when ready)
-  unsigned long long *queue;    // kLevels ready queues of ntask slots each (level kLevels-1 = most critical)
+  unsigned long long *queue;    // kLevels ready queues (level kLevels-1 = most critical); level l
+                                // owns slots [qoff[l], qoff[l+1]) = one per task of that level
+  int qoff[kLevels + 1];
   int *ctrl;                    // kCtrl* counters
   int epoch;
   int nctas;
@@ -984,7 +986,7 @@ __device__ __forceinline__ void st_release64(unsigned long long *p, unsigned lon
 __device__ __forceinline__ void push_ready(const RunArgs &a, int t) {   // (chained tasks may be queued too)
   const int q = (a.tasks[t].meta >> 16) & 15;
   const int pos = atomicAdd(&a.ctrl[kCtrlTail + 64 * q], 1);
-  st_release64(a.queue + (size_t)q * a.ntask + pos, ((unsigned long long)(unsigned)a.epoch << 32) | (unsigned)t);
+  st_release64(a.queue + a.qoff[q] + pos, ((unsigned long long)(unsigned)a.epoch << 32) | (unsigned)t);
   atomicAdd(&a.ctrl[kCtrlAvail], 1);   // idle CTAs poll this one word instead of every queue
   if (a.trace) a.trace[kTraceWords * (size_t)t + 11] = globaltimer();   // diagnostics: push time
 }
@@ -997,7 +999,7 @@ __device__ __forceinline__ int try_pop(const RunArgs &a, int q) {
   while (h < ld_relaxed(tail)) {
     const int got = atomicCAS(head, h, h + 1);
     if (got == h) {
-      const unsigned long long *slot = a.queue + (size_t)q * a.ntask + h;
+      const unsigned long long *slot = a.queue + a.qoff[q] + h;
       unsigned long long v;
       while (((v = ld_acquire64(slot)) >> 32) != (unsigned)a.epoch) __nanosleep(20);
       return (int)(v & 0xffffffffu);
