@@ -1,9 +1,10 @@
 """Benchmark of the B200 tiled QR hot path (BASELINE.json metric and configs[1]).
 
 A step = one tiled QR factorization of the configs[1] matrix (8000 x 2000 fp64,
-i.i.d. N(0,1), p=40 x q=10 tiles of nb=200, ib=32, TT kernels) with EACH tree
-in turn: FlatTree (Sameh-Kuck), Fibonacci, Greedy, PlasmaTree BS=1,5,10,20.
-value = 2n^2(m-n/3) flops x trees x ranks / device time (GFLOP/s).
+i.i.d. N(0,1), p=40 x q=10 tiles of nb=200, ib=32) with EACH tree in turn —
+FlatTree (Sameh-Kuck), Fibonacci, Greedy, PlasmaTree BS=1,5,10,20 — and each
+kernel family (TT and TS, Algorithms 3 and 2).
+value = 2n^2(m-n/3) flops x cases x ranks / device time (GFLOP/s).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
@@ -28,10 +29,12 @@ P, Q, NB, IB = 40, 10, 200, 32
 M, N = P * NB, Q * NB
 TREES = [("flat", 1), ("fibonacci", 1), ("greedy", 1), ("plasma", 1), ("plasma", 5), ("plasma", 10),
          ("plasma", 20)]
+FAMILIES = ("TT", "TS")          # north_star: "executed with TT (triangle-on-triangle) and TS tile kernels"
+CASES = [(t, b, f) for f in FAMILIES for (t, b) in TREES]
 FLOPS = 2.0 * N * N * (M - N / 3.0)
 METRIC = "tiled QR fp64 GFLOP/s (2n²(m−n/3)) and % of B200 FP64 tensor peak, 1/2/4/8 GPU"
 WORKLOAD = ("configs[1]: fp64 tiled QR 8000x2000 (p=40 x q=10 tiles, nb=200, ib=32), i.i.d. N(0,1), "
-            "TT kernels, each tree in turn: flat, fibonacci, greedy, plasma BS=1,5,10,20")
+            "each tree in turn (flat, fibonacci, greedy, plasma BS=1,5,10,20) with TT and with TS kernels")
 SEED = 2024
 
 
@@ -181,12 +184,12 @@ def run_gpu(args, rank, world, local_rank):
 
     def factor_all(times):
         with torch.cuda.stream(stream):
-            for ti, (tree, bs) in enumerate(TREES):
+            for ti, (tree, bs, fam) in enumerate(CASES):
                 A.copy_(A0)                      # restore input; the 128 MB copy also flushes L2
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                tq.tiled_qr(A, M, N, NB, IB, tree, bs, "TT", T=T, stream=stream)
+                tq.tiled_qr(A, M, N, NB, IB, tree, bs, fam, T=T, stream=stream)
                 e1.record(stream)
                 times.append((ti, e0, e1))
 
@@ -207,7 +210,7 @@ def run_gpu(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
     launches_per = tq.last_launch_count()
-    per_tree = np.zeros(len(TREES))
+    per_tree = np.zeros(len(CASES))
     for ti, e0, e1 in ev:
         per_tree[ti] += e0.elapsed_time(e1)
     dev_ms = float(per_tree.sum())                       # device time of all factorizations
@@ -216,7 +219,7 @@ def run_gpu(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
     ms_per_step = max_ms / args.steps
-    total_flops = FLOPS * len(TREES) * args.steps * world
+    total_flops = FLOPS * len(CASES) * args.steps * world
     value = total_flops / (max_ms / 1e3) / 1e9
 
     # end to end through the public API on host buffers (pinned): every factorization
@@ -231,9 +234,9 @@ def run_gpu(args, rank, world, local_rank):
     def e2e_run(nsteps):
         c = 0
         for _ in range(nsteps):
-            for (tree, bs) in TREES:
+            for (tree, bs, fam) in CASES:
                 R_o, T_o = outs[c & 1]
-                tq.tiled_qr_host_async(pin_A.numpy(), R_o.numpy(), T_o.numpy(), M, N, NB, IB, tree, bs, "TT",
+                tq.tiled_qr_host_async(pin_A.numpy(), R_o.numpy(), T_o.numpy(), M, N, NB, IB, tree, bs, fam,
                                        stream=stream)
                 c += 1
         tq.host_wait()
@@ -250,14 +253,14 @@ def run_gpu(args, rank, world, local_rank):
     t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_value = FLOPS * len(TREES) * e2e_steps * world / (float(t.item()) / 1e3) / 1e9
-    h2d = M * N * 8 * len(TREES)
-    d2h = (M * N + tq.t_size(M, N, NB, IB)) * 8 * len(TREES)
+    e2e_value = FLOPS * len(CASES) * e2e_steps * world / (float(t.item()) / 1e3) / 1e9
+    h2d = M * N * 8 * len(CASES)
+    d2h = (M * N + tq.t_size(M, N, NB, IB)) * 8 * len(CASES)
 
     if rank != 0:
         return
     peak, peak_src = fp64_peak()
-    avg_launch_ms = dev_ms / (args.steps * len(TREES))
+    avg_launch_ms = dev_ms / (args.steps * len(CASES))
     achieved = FLOPS / (avg_launch_ms / 1e3) / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
@@ -268,7 +271,8 @@ def run_gpu(args, rank, world, local_rank):
                    "l2": "input restored by a 128 MB device copy before every factorization (outside the "
                          "events; flushes L2); the matrix itself (128 MB) exceeds L2",
                    "timing": "CUDA events around each tiled_qr launch on its stream, summed; max over ranks"},
-        "per_tree_gflops": {f"{t}:{b}": FLOPS * args.steps / (ms / 1e3) / 1e9 for (t, b), ms in zip(TREES, per_tree)},
+        "per_tree_gflops": {f"{t}:{b} {f}": FLOPS * args.steps / (ms / 1e3) / 1e9
+                            for (t, b, f), ms in zip(CASES, per_tree)},
         "fp64_peak_frac": achieved / peak,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(), "kernel": "tqr_persistent",
@@ -278,7 +282,7 @@ def run_gpu(args, rank, world, local_rank):
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "tiled_qr_host_async (pinned host buffers; per factorization H2D A, factor, D2H A and T; "
                        "copies pipelined with neighbouring factorizations; CUDA events incl. the final wait)"},
-        "gpu_launches": launches_per * len(TREES) * args.steps,
+        "gpu_launches": launches_per * len(CASES) * args.steps,
     }
     if not args.no_cpu_baseline and world == 1:
         budget = float(os.environ.get("TQR_CPU_BUDGET_S", "15"))
@@ -368,6 +372,52 @@ def run_tall(args, rank, world, local_rank):
     }), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# configs[4]: q-sweep at fixed height p = 40, nb = 200 (the paper's experiment
+# grid, §4), every tree, TT and TS kernels; one JSON line with
+# the per-(q, tree, family) GFLOP/s table (a report, not the bench headline)
+# ---------------------------------------------------------------------------
+def run_qsweep(args, local_rank):
+    import torch
+    import paper_1104_4475_b200 as tq
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    p, nb, ib = 40, 200, 32
+    qs = [1, 2, 4, 8, 16, 24, 32, 40]
+    trees = [("flat", 1), ("fibonacci", 1), ("greedy", 1), ("asap", 1), ("plasma", 1), ("plasma", 5),
+             ("plasma", 10), ("plasma", 20)]
+    g = torch.Generator(device=dev).manual_seed(SEED)
+    table = {}
+    for q in qs:
+        m, n = p * nb, q * nb
+        flops = 2.0 * n * n * (m - n / 3.0)
+        A0 = torch.randn(m * n, dtype=torch.float64, device=dev, generator=g)
+        A = torch.empty_like(A0)
+        T = torch.zeros(tq.t_size(m, n, nb, ib), dtype=torch.float64, device=dev)
+        for fam in ("TT", "TS"):
+            for (tree, bs) in trees:
+                if tree == "asap" and fam == "TS":
+                    continue
+                best = None
+                for it in range(2 + max(1, args.steps)):
+                    A.copy_(A0)
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    tq.tiled_qr(A, m, n, nb, ib, tree, bs if tree != "asap" else q, fam, T=T)
+                    e1.record()
+                    e1.synchronize()
+                    if it >= 2:
+                        ms = e0.elapsed_time(e1)
+                        best = ms if best is None else min(best, ms)
+                table[f"q={q} {tree}:{bs} {fam}"] = round(flops / (best / 1e3) / 1e9, 1)
+        del A0, A, T
+    print(json.dumps({"workload": "configs[4]: q-sweep p=40, nb=200, ib=32, i.i.d. N(0,1); GFLOP/s, best of "
+                                  f"{max(1, args.steps)} timed runs (CUDA events) per case",
+                      "unit": "GFLOP/s", "gflops": table}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -375,8 +425,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="square", choices=["square", "tall"],
-                    help="square = configs[1] (default); tall = configs[3] partitioned over the ranks")
+    ap.add_argument("--workload", default="square", choices=["square", "tall", "qsweep"],
+                    help="square = configs[1] (default); tall = configs[3] partitioned over the ranks; "
+                         "qsweep = configs[4] table (1 GPU)")
     ap.add_argument("--tree", default="greedy", help="tree of the local factorizations (tall workload)")
     ap.add_argument("--tall-p", type=int, default=0, help="override p of the tall workload (testing)")
     args = ap.parse_args()
@@ -385,6 +436,10 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.workload == "qsweep":
+        if rank == 0:
+            run_qsweep(args, local_rank)
         return
     if world > 1:
         import torch
