@@ -59,8 +59,9 @@ enum tqr_tree {
                          reduction of tall-skinny matrices: the
                          input's diagonal tiles count as triangles, tiles below
                          them as structural zeros (they must hold zeros). */
-  TQR_ASAP = 6,       /* ASAP, lines 666-682: eliminations decided during the
-                         tiled execution (start as soon as two rows are ready) */
+  TQR_ASAP = 6,       /* ASAP, lines 666-682: eliminations decided while the
+                         tiled algorithm runs: one starts as soon as two rows
+                         are ready */
   TQR_GRASAP = 7      /* Grasap(k), lines 685-692: Greedy on columns 1..q-k,
                          ASAP on the last k columns; k is passed as `bs` */
 };

@@ -175,21 +175,23 @@ def test_repeat_launch_epochs():
         compare_with_oracle(A, nb, ib, "greedy", 1, "TT")
 
 
-@pytest.mark.parametrize("tree,bs", [("greedy", 1), ("fibonacci", 1), ("flat", 1), ("plasma", 5)])
-def test_config1_full_size_properties(tree, bs):
+@pytest.mark.parametrize("tree,bs,family", [("greedy", 1, "TT"), ("fibonacci", 1, "TT"), ("flat", 1, "TT"),
+                                            ("plasma", 5, "TT"), ("flat", 1, "TS"), ("plasma", 10, "TS"),
+                                            ("asap", 10, "TT")])
+def test_config1_full_size_properties(tree, bs, family):
     """configs[1] at full size in the bench's launch configuration: 8000 x 2000,
     nb = 200, ib = 32. The oracle cannot factor it in seconds, so check
     properties that hold at any size plus LAPACK's R (a library special case)."""
     p, q, nb, ib = 40, 10, 200, 32
     m, n = p * nb, q * nb
     A = qrinputs.gaussian(m, n, 2024)
-    buf, T = run_gpu(A, nb, ib, tree, bs, "TT")
+    buf, T = run_gpu(A, nb, ib, tree, bs, family)
     got = qrinputs.from_tiles(buf.cpu().numpy(), p, q, nb)
     R = np.triu(got[:n, :n])
     Rl = np.linalg.qr(A, mode="r")
     assert rel(nu.sign_normalise(R), nu.sign_normalise(Rl)) <= TOL_R
     # A - QR and orthogonality on the device, through apply_q
-    Q = gpu_Q(buf, T, m, n, nb, ib, tree, bs, "TT")
+    Q = gpu_Q(buf, T, m, n, nb, ib, tree, bs, family)
     assert np.linalg.norm(A - Q @ R) / np.linalg.norm(A) <= TOL_QR
     assert np.linalg.norm(np.eye(n) - Q.T @ Q) <= TOL_QR
 

@@ -13,8 +13,9 @@ import paper_1104_4475_b200 as tq  # noqa: E402
 
 a = sys.argv[1:]
 p, q, nb, ib = (int(x) for x in (a[:4] if len(a) >= 4 else (40, 10, 200, 32)))
-tree, bs = ((a[4] if len(a) > 4 else "greedy").split(":") + ["1"])[:2]
-bs = int(bs)
+spec = (a[4] if len(a) > 4 else "greedy").split(":")
+tree, bs = spec[0], int(spec[1]) if len(spec) > 1 else 1
+family = spec[2] if len(spec) > 2 else "TT"
 m, n = p * nb, q * nb
 g = torch.Generator(device="cuda").manual_seed(0)
 A0 = torch.randn(m * n, dtype=torch.float64, device="cuda", generator=g)
@@ -26,7 +27,7 @@ for it in range(3):
         tq.trace_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    tq.tiled_qr(A, m, n, nb, ib, tree, bs, "TT", T=T)
+    tq.tiled_qr(A, m, n, nb, ib, tree, bs, family, T=T)
     e1.record()
     torch.cuda.synchronize()
 tq.trace_enable(False)
@@ -39,7 +40,7 @@ span = (tr["done"].max() - t0) / 1e3
 run = (tr["done"] - tr["ready"]) / 1e3
 wait = (tr["ready"] - tr["taken"]) / 1e3
 nsm = len(np.unique(tr["sm"]))
-print(f"{tree}:{bs} p={p} q={q} nb={nb} ib={ib}: event {ms:.3f} ms, traced span {span / 1e3:.3f} ms, "
+print(f"{tree}:{bs}:{family} p={p} q={q} nb={nb} ib={ib}: event {ms:.3f} ms, traced span {span / 1e3:.3f} ms, "
       f"{len(tr)} tasks on {nsm} SMs")
 print(f"  busy (sum run) / (SMs x span) = {run.sum() / (nsm * span):.3f};  waiting share = {wait.sum() / (nsm * span):.3f}")
 unit = nb ** 3 / 3.0
