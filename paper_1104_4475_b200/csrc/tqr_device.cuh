@@ -22,9 +22,11 @@ constexpr size_t kMaxSmem = 227 * 1024 - 512;   // dynamic smem budget (opt-in m
 constexpr int kTld = 33;
 constexpr int kTraceWords = 12;             // per-task trace record (diagnostics)
 // scheduler control words (ints; each on its own 128-byte line): per priority
-// level l a queue head at kCtrlHead + 64 l and tail at kCtrlTail + 64 l
+// level l a queue head at kCtrlHead + 64 l, its tail at kCtrlTail + 64 l and
+// its count of published, unclaimed tasks at kCtrlLevel + 32 l
 constexpr int kCtrlHead = 0, kCtrlTail = 32, kCtrlDone = 64 * kLevels, kCtrlExit = 64 * kLevels + 32,
-              kCtrlAvail = 64 * kLevels + 64, kCtrlWords = 64 * kLevels + 96;                    // ld of the 32 x 32 smem T / top / G blocks
+              kCtrlLevel = 64 * kLevels + 96,
+              kCtrlWords = 96 * kLevels + 96;
 constexpr int kPanelScratch = 2 * 32 * kTld + 2 * 256 + 8 + 32;
 
 struct RunArgs {
@@ -987,26 +989,24 @@ __device__ __forceinline__ void push_ready(const RunArgs &a, int t) {   // (chai
   const int q = (a.tasks[t].meta >> 16) & 15;
   const int pos = atomicAdd(&a.ctrl[kCtrlTail + 64 * q], 1);
   st_release64(a.queue + a.qoff[q] + pos, ((unsigned long long)(unsigned)a.epoch << 32) | (unsigned)t);
-  atomicAdd(&a.ctrl[kCtrlAvail], 1);   // idle CTAs poll this one word instead of every queue
+  atomicAdd(&a.ctrl[kCtrlLevel + 32 * q], 1);
   if (a.trace) a.trace[kTraceWords * (size_t)t + 11] = globaltimer();   // diagnostics: push time
 }
 
-// claim the next slot of queue q if one is published; returns the task or -1
+// Claim a task of queue q, or return -1. A fetch-and-subtract on the level's
+// count reserves one published task (undone if the count was not positive),
+// then a fetch-and-add on the head takes the next slot; neither retries, so
+// tens of idle CTAs claiming from one level do not serialise on a CAS loop.
+// The slot's pusher has already taken its tail position, so at worst the pop
+// waits for that store to land.
 __device__ __forceinline__ int try_pop(const RunArgs &a, int q) {
-  int *head = &a.ctrl[kCtrlHead + 64 * q];
-  const int *tail = &a.ctrl[kCtrlTail + 64 * q];
-  int h = ld_relaxed(head);
-  while (h < ld_relaxed(tail)) {
-    const int got = atomicCAS(head, h, h + 1);
-    if (got == h) {
-      const unsigned long long *slot = a.queue + a.qoff[q] + h;
-      unsigned long long v;
-      while (((v = ld_acquire64(slot)) >> 32) != (unsigned)a.epoch) __nanosleep(20);
-      return (int)(v & 0xffffffffu);
-    }
-    h = got;
-  }
-  return -1;
+  int *cnt = &a.ctrl[kCtrlLevel + 32 * q];
+  if (atomicSub(cnt, 1) <= 0) { atomicAdd(cnt, 1); return -1; }
+  const int h = atomicAdd(&a.ctrl[kCtrlHead + 64 * q], 1);
+  const unsigned long long *slot = a.queue + a.qoff[q] + h;
+  unsigned long long v;
+  while (((v = ld_acquire64(slot)) >> 32) != (unsigned)a.epoch) __nanosleep(20);
+  return (int)(v & 0xffffffffu);
 }
 
 __device__ __forceinline__ unsigned ld_acquire_u(const unsigned *p) {
@@ -1033,24 +1033,36 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
   if (threadIdx.x == 0)
     for (int r = blockIdx.x; r < a.nroots; r += gridDim.x) push_ready(a, a.roots[r]);
   for (;;) {
-    if (threadIdx.x == 0) {
-      unsigned long long t_take = a.trace ? globaltimer() : 0ull;
+    if (threadIdx.x < 32) {
+      // warp 0 claims the next task: lane l < kLevels reads level l's count,
+      // a ballot names the non-empty levels, lane 0 claims from the highest
+      const int lane = threadIdx.x;
+      __syncwarp();   // s_chain was written by lane 0 at the end of the last task
+      unsigned long long t_take = (a.trace && lane == 0) ? globaltimer() : 0ull;
       int t = s_chain;
       if (t < 0) {
-        s_resident = 0;
+        if (lane == 0) s_resident = 0;
         unsigned backoff = 32;
         for (;;) {
-          if (ld_relaxed(&a.ctrl[kCtrlAvail]) > 0) {
-            for (int q = kLevels - 1; q >= 0 && t < 0; --q) t = try_pop(a, q);
-            if (t >= 0) { atomicSub(&a.ctrl[kCtrlAvail], 1); break; }
+          const int c = lane < kLevels ? ld_relaxed(&a.ctrl[kCtrlLevel + 32 * lane]) : 0;
+          unsigned live = __ballot_sync(0xffffffffu, c > 0);
+          while (live && t < 0) {
+            const int q = 31 - __clz(live);
+            int got = -1;
+            if (lane == 0) got = try_pop(a, q);
+            t = __shfl_sync(0xffffffffu, got, 0);
+            live &= ~(1u << q);
           }
-          if (ld_relaxed(&a.ctrl[kCtrlDone]) >= a.ntask) { t = -1; break; }
+          if (t >= 0) break;
+          int fin = 0;
+          if (lane == 0) fin = ld_relaxed(&a.ctrl[kCtrlDone]) >= a.ntask;
+          if (__shfl_sync(0xffffffffu, fin, 0)) { t = -1; break; }
           __nanosleep(backoff);
           backoff = backoff < 1024 ? backoff * 2 : 1024;
         }
       }
-      s_task = t;
-      if (a.trace && t >= 0) {
+      if (lane == 0) s_task = t;
+      if (lane == 0 && a.trace && t >= 0) {
         a.trace[kTraceWords * (size_t)t] = t_take;
         a.trace[kTraceWords * (size_t)t + 1] = globaltimer();
         for (int x = 0; x < 8; ++x) s_prof[x] = 0;
@@ -1096,8 +1108,9 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
   if (threadIdx.x == 0) {
     const int n = atomicAdd(&a.ctrl[kCtrlExit], 1);
     if (n == a.nctas - 1) {
-      for (int q = 0; q < kLevels; ++q) a.ctrl[kCtrlHead + 64 * q] = a.ctrl[kCtrlTail + 64 * q] = 0;
-      a.ctrl[kCtrlDone] = 0; a.ctrl[kCtrlExit] = 0; a.ctrl[kCtrlAvail] = 0;
+      for (int q = 0; q < kLevels; ++q)
+        a.ctrl[kCtrlHead + 64 * q] = a.ctrl[kCtrlTail + 64 * q] = a.ctrl[kCtrlLevel + 32 * q] = 0;
+      a.ctrl[kCtrlDone] = 0; a.ctrl[kCtrlExit] = 0;
       __threadfence();
     }
   }
