@@ -28,5 +28,5 @@ for spec in trees:
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     best = min(ts[1:])
-    print(f"{tree}:{bs} p={p} q={q} nb={nb}: {best:.3f} ms  {flops / best / 1e9:.1f} GFLOP/s  (all {['%.2f' % t for t in ts]})",
+    print(f"{tree}:{bs} p={p} q={q} nb={nb}: {best:.3f} ms  {flops / best / 1e9:.1f} TFLOP/s  (all {['%.2f' % t for t in ts]})",
           flush=True)
