@@ -1078,12 +1078,19 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
     run_task(a, tk, smem, L, s_resident != 0, mbph);
     __syncthreads();
     prof_mark(PH_STORE);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
+      // release the successors, one per lane (a panel block can have tens):
+      // every lane fences the CTA's writes (ordered by the barrier above) to
+      // gpu scope before its arrival, so the atomics run in parallel instead
+      // of as a dependent chain of round trips on one thread
       __threadfence();
-      for (int x = tk.dep_begin; x < tk.dep_end; ++x) {
+      for (int x = tk.dep_begin + (int)threadIdx.x; x < tk.dep_end; x += 32) {
         const int sc = a.succ[x];
         if (atom_add_acqrel(a.cnt + sc, 1u) + 1u == need_count(a, sc)) push_ready(a, sc);
       }
+      __syncwarp();
+    }
+    if (threadIdx.x == 0) {
       if (a.trace) {
         unsigned long long *tr = a.trace + kTraceWords * (size_t)t;
         tr[2] = globaltimer();
