@@ -45,6 +45,7 @@ struct RunArgs {
   double *A, *T, *C;
   int p, q, nb, ib, ws, trans;
   int tma;                     // 1: move C strips and V blocks with 1-D TMA bulk copies
+  int work_first;              // 1: a CTA runs the most urgent successor it made ready (not queued)
   unsigned long long *trace;   // optional: kTraceWords u64 per task (taken, ready, done, smid<<32|kind, 8 phase cycle counters)
 };
 
@@ -1078,15 +1079,45 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
     run_task(a, tk, smem, L, s_resident != 0, mbph);
     __syncthreads();
     prof_mark(PH_STORE);
+    int keep = -1;   // (lane 0) successor this CTA runs next without queueing it
     if (threadIdx.x < 32) {
       // release the successors, one per lane (a panel block can have tens):
       // every lane fences the CTA's writes (ordered by the barrier above) to
       // gpu scope before its arrival, so the atomics run in parallel instead
       // of as a dependent chain of round trips on one thread
+      const int lane = threadIdx.x;
       __threadfence();
-      for (int x = tk.dep_begin + (int)threadIdx.x; x < tk.dep_end; x += 32) {
+      // work-first: without a chain continuation, the CTA keeps the most
+      // urgent successor it made ready if no queued task is more urgent
+      // (the queue probe is issued alongside the arrivals)
+      const bool may_keep = tk.chain < 0 && a.work_first;
+      const int qc = (may_keep && lane < kLevels) ? ld_relaxed(&a.ctrl[kCtrlLevel + 32 * lane]) : 0;
+      int mine = -1, mine_lvl = -1;
+      for (int x = tk.dep_begin + lane; x < tk.dep_end; x += 32) {
         const int sc = a.succ[x];
-        if (atom_add_acqrel(a.cnt + sc, 1u) + 1u == need_count(a, sc)) push_ready(a, sc);
+        const int m = a.tasks[sc].meta;
+        const unsigned need = (unsigned)a.epoch * (unsigned)((m & 0xffff) + ((m >> 20) & 1));
+        if (atom_add_acqrel(a.cnt + sc, 1u) + 1u == need) {
+          const int lvl = (m >> 16) & 15;
+          if (may_keep && lvl > mine_lvl) {
+            if (mine >= 0) push_ready(a, mine);
+            mine = sc; mine_lvl = lvl;
+          } else {
+            push_ready(a, sc);
+          }
+        }
+      }
+      if (may_keep) {
+        const unsigned live = __ballot_sync(0xffffffffu, qc > 0);
+        const int qmax = live ? 31 - __clz(live) : -1;
+        int best = mine >= 0 ? mine_lvl * 32 + lane : -1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+        const bool win = best >= 0 && (best & 31) == lane && mine_lvl >= qmax;
+        if (mine >= 0 && !win) push_ready(a, mine);
+        const unsigned wl = __ballot_sync(0xffffffffu, win);
+        keep = __shfl_sync(0xffffffffu, mine, wl ? __ffs(wl) - 1 : 0);
+        if (!wl) keep = -1;
       }
       __syncwarp();
     }
@@ -1109,7 +1140,7 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
         if (atom_add_acqrel(a.cnt + c, 1u) + 1u == need) nxt = c;
       }
       s_resident = (nxt >= 0 && is_panel_block(tk.kind)) ? 1 : 0;
-      s_chain = nxt;
+      s_chain = nxt >= 0 ? nxt : keep;
     }
   }
   if (threadIdx.x == 0) {
