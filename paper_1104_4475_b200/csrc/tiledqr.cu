@@ -297,6 +297,7 @@ static int launch(DevPlan *pl, int p, int q, int nb, int ib, double *A, double *
   a.p = p; a.q = q; a.nb = nb; a.ib = ib; a.ws = pl->ws; a.trans = trans;
   a.tma = env_int("TQR_TMA", 0);   // 1-D TMA bulk path (measured ~4% slower than cp.async here)
   a.work_first = env_int("TQR_WORK_FIRST", 1) != 0;
+  a.chain_spin = env_int("TQR_CHAIN_SPIN", 0);   // measured best: no spin (profiles/r01_chain_spin_sweep.txt)
   a.trace = nullptr;
   if (g_trace_on) {
     if (!pl->trace) CUDA_TRY(cudaMalloc(&pl->trace, sizeof(unsigned long long) * kTraceWords * pl->ntask));

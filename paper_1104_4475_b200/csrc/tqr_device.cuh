@@ -46,6 +46,7 @@ struct RunArgs {
   int p, q, nb, ib, ws, trans;
   int tma;                     // 1: move C strips and V blocks with 1-D TMA bulk copies
   int work_first;              // 1: a CTA runs the most urgent successor it made ready (not queued)
+  int chain_spin;              // polls (128 ns apart) for a chained successor's other inputs
   unsigned long long *trace;   // optional: kTraceWords u64 per task (taken, ready, done, smid<<32|kind, 8 phase cycle counters)
 };
 
@@ -1136,7 +1137,7 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
       if (tk.chain >= 0) {
         const int c = tk.chain;
         const unsigned need = need_count(a, c);
-        for (int it = 0; it < 64 && ld_acquire_u(a.cnt + c) + 1u < need; ++it) __nanosleep(128);
+        for (int it = 0; it < a.chain_spin && ld_acquire_u(a.cnt + c) + 1u < need; ++it) __nanosleep(128);
         if (atom_add_acqrel(a.cnt + c, 1u) + 1u == need) nxt = c;
       }
       s_resident = (nxt >= 0 && is_panel_block(tk.kind)) ? 1 : 0;
