@@ -963,7 +963,8 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
 // Dataflow with per-task dependency counters (north_star: "a persistent kernel
 // gated by per-tile dependency counters"). A finished task bumps the counter
 // of each successor (atom.acq_rel); the predecessor that completes a
-// successor's count pushes it on one of two ready queues (panel chain first).
+// successor's count pushes it on the ready queue of its priority level (or
+// runs it next itself: chain continuation / work-first).
 // CTAs only ever take ready tasks, so no CTA idles on a specific task while
 // others are runnable. Queue slots carry the launch epoch, counters
 // accumulate epoch x indegree, and the last CTA to leave resets the queue
