@@ -312,3 +312,33 @@ def test_host_async_pipeline():
         got = qrinputs.from_tiles(R_o.numpy(), p, q, nb)
         assert rel(got, F.A) <= TOL_R
         assert rel(T_o.numpy()[: F.T.size], F.T) <= TOL_R
+
+
+SCHED_MODES = [{}, {"TQR_WORK_FIRST": "0"}, {"TQR_CHAIN_SPIN": "64"}, {"TQR_PRIO": "1"}, {"TQR_PRIO": "3"},
+               {"TQR_LEVELS": "2"}, {"TQR_LOOKAHEAD": "0"}, {"TQR_GRID": "5"}, {"TQR_GRID": "1"}, {"TQR_TMA": "1"}]
+
+
+@pytest.mark.parametrize("tree,bs,family", [("greedy", 1, "TT"), ("plasma", 3, "TS"), ("asap", 1, "TT")])
+def test_schedule_invariance(tree, bs, family, monkeypatch):
+    """The schedule never changes the arithmetic: every tile is updated by the
+    same tasks in the order the graph fixes, so A (R and V) and T must be
+    bitwise identical under every scheduling mode (claim order, work-first,
+    chain spin, priority rule, number of levels, grid of 1 or 5 CTAs)."""
+    p, q, nb, ib = 9, 4, 72, 32
+    m, n = p * nb, q * nb
+    A = qrinputs.gaussian(m, n, 77)
+    ref = None
+    for mode in SCHED_MODES:
+        for k in ("TQR_WORK_FIRST", "TQR_CHAIN_SPIN", "TQR_PRIO", "TQR_LEVELS", "TQR_LOOKAHEAD", "TQR_GRID", "TQR_TMA"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in mode.items():
+            monkeypatch.setenv(k, v)
+        buf, T = run_gpu(A, nb, ib, tree, bs, family)
+        got = (buf.cpu().numpy(), T.cpu().numpy())
+        if ref is None:
+            ref = got
+            # and the default schedule is itself correct (vs LAPACK's R)
+            R = np.triu(qrinputs.from_tiles(got[0], p, q, nb)[:n, :n])
+            assert rel(nu.sign_normalise(R), nu.sign_normalise(np.linalg.qr(A, mode="r"))) <= TOL_R
+        else:
+            assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1]), mode
