@@ -161,6 +161,10 @@ static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, in
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   int ws = pick_ws(nb, ib);
+  if (smem_bytes(nb, ib, ws) > kMaxSmem)
+    return fail(TQR_EUNSUP, "strip width " + std::to_string(ws) + " (TQR_WS) needs " +
+                                std::to_string(smem_bytes(nb, ib, ws)) + " bytes of shared memory for nb = " +
+                                std::to_string(nb) + "; at most " + std::to_string(kMaxSmem) + " fit");
   PlanKey key{dev, mode, p, q, qc, nb, ib, tree, bs, family,
               (ws * 4 + (env_int("TQR_SPLIT", 1) != 0) * 2 + (env_int("TQR_LOOKAHEAD", 1) != 0)) * 64 +
                   env_int("TQR_LEVELS", kLevels) + 4096 * env_int("TQR_PRIO", 0)};

@@ -342,3 +342,13 @@ def test_schedule_invariance(tree, bs, family, monkeypatch):
             assert rel(nu.sign_normalise(R), nu.sign_normalise(np.linalg.qr(A, mode="r"))) <= TOL_R
         else:
             assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1]), mode
+
+
+def test_strip_width_too_wide_is_rejected(monkeypatch):
+    """A forced strip width whose C strip does not fit in shared memory fails
+    with TQR_EUNSUP and a message, before any launch."""
+    monkeypatch.setenv("TQR_WS", "64")
+    p, q, nb = 4, 2, 200
+    A = torch.zeros(p * q * nb * nb, dtype=torch.float64, device=DEV)
+    with pytest.raises(tq.TiledQRError, match="shared memory"):
+        tq.tiled_qr(A, p * nb, q * nb, nb, 32, "greedy")
