@@ -167,7 +167,23 @@ __device__ __forceinline__ void async_block(double *dst, int lds, const double *
   const double *g = src + r0 + (size_t)c0 * ldg;
   const bool v16 = ((nr | lds | ldg) & 1) == 0 && ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (v16) {          // warps over columns, lanes over 16-byte row pairs (no integer division)
+  if (v16 && nr <= 4 * 64 && ncol <= 4 * kWarps) {
+    // warps over columns, lanes over 16-byte row pairs; nr <= 256 and ncol <= 32
+    // always hold here (nb <= kMaxNb), so both loops unroll into predicated
+    // copies with constant offsets from one base address per thread
+    double *d0 = dst + 2 * lane + warp * lds;
+    const double *g0 = g + 2 * lane + (size_t)warp * ldg;
+#pragma unroll
+    for (int ci = 0; ci < 4; ++ci) {
+      if (warp + ci * kWarps < ncol) {
+        double *d = d0 + ci * kWarps * lds;
+        const double *gs = g0 + (size_t)ci * kWarps * ldg;
+#pragma unroll
+        for (int ri = 0; ri < 4; ++ri)
+          if (2 * lane + 64 * ri < nr) cp_async16(d + 64 * ri, gs + 64 * ri);
+      }
+    }
+  } else if (v16) {   // warps over columns, lanes over 16-byte row pairs (no integer division)
     for (int c = warp; c < ncol; c += kWarps)
       for (int r = 2 * lane; r < nr; r += 64) cp_async16(dst + r + c * lds, g + r + (size_t)c * ldg);   // dst row 0 = r0
   } else {
@@ -245,7 +261,23 @@ __device__ __forceinline__ void load_rows(double *buf, int ldc, int off, const d
 __device__ __forceinline__ void store_rows(const double *buf, int ldc, int off, double *tile, int nb,
                                            int r0, int r1, int c0, int wsz) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if ((((r1 - r0) | ldc | nb | r0 | off) & 1) == 0) {
+  if ((((r1 - r0) | ldc | nb | r0 | off) & 1) == 0 && r1 - r0 <= 4 * 64 && wsz <= 4 * kWarps) {
+    // same unrolled, predicated form as async_block (rows <= 256, columns <= 32)
+    const int nr = r1 - r0;
+    const double *b0 = buf + off + r0 + 2 * lane + warp * ldc;
+    double *t0 = tile + r0 + 2 * lane + (size_t)(c0 + warp) * nb;
+#pragma unroll
+    for (int ci = 0; ci < 4; ++ci) {
+      if (warp + ci * kWarps < wsz) {
+        const double *b = b0 + ci * kWarps * ldc;
+        double *tt = t0 + (size_t)ci * kWarps * nb;
+#pragma unroll
+        for (int ri = 0; ri < 4; ++ri)
+          if (2 * lane + 64 * ri < nr)
+            *reinterpret_cast<double2 *>(tt + 64 * ri) = *reinterpret_cast<const double2 *>(b + 64 * ri);
+      }
+    }
+  } else if ((((r1 - r0) | ldc | nb | r0 | off) & 1) == 0) {
     for (int c = warp; c < wsz; c += kWarps)
       for (int r = r0 + 2 * lane; r < r1; r += 64)
         *reinterpret_cast<double2 *>(tile + r + (size_t)(c0 + c) * nb) =
