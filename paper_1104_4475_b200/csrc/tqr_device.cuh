@@ -294,18 +294,17 @@ __device__ __forceinline__ void store_rows(const double *buf, int ldc, int off, 
 __device__ __forceinline__ void issue_v_geqrt(double *V, int ldv, const double *X, int nb, int j0, int bw) {
   async_block(V, ldv, X, nb, j0, nb, j0, bw);
 }
+// (bw <= 32: the column loops unroll into 4 predicated steps per warp)
 __device__ __forceinline__ void fix_v_geqrt(double *V, int ldv, int nb, int j0, int bw) {
-  const int nr = nb - j0, nr4 = (nr + 15) & ~15;
-  {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int l = warp; l < bw; l += kWarps)
+  const int nr = nb - j0, pad = ((nr + 15) & ~15) - nr;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int li = 0; li < 4; ++li) {
+    const int l = warp + li * kWarps;
+    if (l < bw) {
       if (lane <= l && lane < nr) V[lane + l * ldv] = lane == l ? 1.0 : 0.0;
-  }
-  const int pad = nr4 - nr;
-  if (pad > 0) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int l = warp; l < bw; l += kWarps)
       if (lane < pad) V[nr + lane + l * ldv] = 0.0;
+    }
   }
 }
 // V2 of a TTQRT (tri) / TSQRT block: rows 0..R2-1 of tile X, R2 = j0+bw (TT) or nb (TS);
@@ -314,17 +313,15 @@ __device__ __forceinline__ void issue_v_tp(double *V, int ldv, const double *X, 
   async_block(V, ldv, X, nb, 0, tri ? j0 + bw : nb, j0, bw);
 }
 __device__ __forceinline__ void fix_v_tp(double *V, int ldv, int nb, int j0, int bw, bool tri) {
-  const int nr = tri ? j0 + bw : nb, nr4 = (nr + 15) & ~15;
-  if (tri) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int l = warp; l < bw; l += kWarps)
-      if (lane > l && lane < bw) V[j0 + lane + l * ldv] = 0.0;
-  }
-  const int pad = nr4 - nr;
-  if (pad > 0) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int l = warp; l < bw; l += kWarps)
+  const int nr = tri ? j0 + bw : nb, pad = ((nr + 15) & ~15) - nr;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int li = 0; li < 4; ++li) {
+    const int l = warp + li * kWarps;
+    if (l < bw) {
+      if (tri && lane > l && lane < bw) V[j0 + lane + l * ldv] = 0.0;
       if (lane < pad) V[nr + lane + l * ldv] = 0.0;
+    }
   }
 }
 // zero V rows [nr, round_up(nr, 16)) of columns 0..bw-1 (K padding of the DMMA loops)
@@ -340,9 +337,13 @@ __device__ __forceinline__ void zero_vpad(double *V, int ldv, int nr, int bw) {
 // the rest of the 32 x 32 block is zeroed (it feeds a padded DMMA)
 __device__ __forceinline__ void issue_t(double *Ts, const double *Tslot, int ib, int j0, int bw) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int c = warp; c < 32; c += kWarps) {
-    if (lane <= c && c < bw) cp_async8(Ts + lane + c * kTld, Tslot + lane + (size_t)(j0 + c) * ib);
-    else Ts[lane + c * kTld] = 0.0;
+  double *d0 = Ts + lane + warp * kTld;
+  const double *g0 = Tslot + lane + (size_t)(j0 + warp) * ib;
+#pragma unroll
+  for (int ci = 0; ci < 4; ++ci) {
+    const int c = warp + ci * kWarps;
+    if (lane <= c && c < bw) cp_async8(d0 + ci * kWarps * kTld, g0 + (size_t)ci * kWarps * ib);
+    else d0[ci * kWarps * kTld] = 0.0;
   }
 }
 
@@ -428,7 +429,8 @@ __device__ void apply_block_t(double *Ctop, double *Cv, int ldc, int nrows, cons
     const int mt = (bw + 15) >> 4;
     const int kpad = (nrows + 15) & ~15;        // V rows [nrows, kpad) are zero
     for (int f = warp; f < mt * nt; f += kWarps) {
-      const int m0 = (f % mt) * 16, n0 = (f / mt) * 8;
+      // bw <= 32, so mt is 1 or 2: no integer division
+      const int m0 = (mt == 2 ? (f & 1) : 0) * 16, n0 = (mt == 2 ? (f >> 1) : f) * 8;
       double acc[4][4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
