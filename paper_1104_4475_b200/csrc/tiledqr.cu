@@ -138,7 +138,9 @@ static int upload(const DevGraph &g, int ws, DevPlan &pl) {
   pl.ws = ws;
   const size_t n1 = pl.ntask ? pl.ntask : 1;
   CUDA_TRY(cudaMalloc(&pl.tasks, sizeof(DevTask) * n1));
-  CUDA_TRY(cudaMalloc(&pl.succ, sizeof(int32_t) * (g.succ.empty() ? 1 : g.succ.size())));
+  // successor edges as (task, that task's meta) pairs: releasing a successor
+  // needs its indegree, and one 8-byte load beats two dependent ones
+  CUDA_TRY(cudaMalloc(&pl.succ, sizeof(int32_t) * 2 * (g.succ.empty() ? 1 : g.succ.size())));
   CUDA_TRY(cudaMalloc(&pl.roots, sizeof(int32_t) * (g.roots.empty() ? 1 : g.roots.size())));
   CUDA_TRY(cudaMalloc(&pl.cnt, sizeof(unsigned) * n1));
   for (int l = 0; l <= kLevels; ++l) pl.qoff[l] = 0;
@@ -147,7 +149,14 @@ static int upload(const DevGraph &g, int ws, DevPlan &pl) {
   CUDA_TRY(cudaMalloc(&pl.queue, sizeof(unsigned long long) * n1));
   CUDA_TRY(cudaMalloc(&pl.ctrl, sizeof(int) * kCtrlWords));
   if (!g.tasks.empty()) CUDA_TRY(cudaMemcpy(pl.tasks, g.tasks.data(), sizeof(DevTask) * g.tasks.size(), cudaMemcpyHostToDevice));
-  if (!g.succ.empty()) CUDA_TRY(cudaMemcpy(pl.succ, g.succ.data(), sizeof(int32_t) * g.succ.size(), cudaMemcpyHostToDevice));
+  if (!g.succ.empty()) {
+    std::vector<int32_t> edges(2 * g.succ.size());
+    for (size_t x = 0; x < g.succ.size(); ++x) {
+      edges[2 * x] = g.succ[x];
+      edges[2 * x + 1] = g.tasks[g.succ[x]].meta;
+    }
+    CUDA_TRY(cudaMemcpy(pl.succ, edges.data(), sizeof(int32_t) * edges.size(), cudaMemcpyHostToDevice));
+  }
   if (!g.roots.empty()) CUDA_TRY(cudaMemcpy(pl.roots, g.roots.data(), sizeof(int32_t) * g.roots.size(), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemset(pl.cnt, 0, sizeof(unsigned) * n1));
   CUDA_TRY(cudaMemset(pl.queue, 0, sizeof(unsigned long long) * n1));
@@ -237,7 +246,11 @@ extern "C" int64_t tqr_trace_graph(int32_t *succ_ptr, int32_t *succ, int64_t cap
   if (cap < ns || cap < (int64_t)pl->ntask + 1) return fail(TQR_ECAP, "tqr_trace_graph: capacity too small");
   for (int t = 0; t < pl->ntask; ++t) succ_ptr[t] = pl->host_tasks[t].dep_begin;
   succ_ptr[pl->ntask] = (int32_t)ns;
-  if (ns) CUDA_TRY(cudaMemcpy(succ, pl->succ, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost));
+  if (ns) {
+    std::vector<int32_t> edges(2 * ns);
+    CUDA_TRY(cudaMemcpy(edges.data(), pl->succ, sizeof(int32_t) * 2 * ns, cudaMemcpyDeviceToHost));
+    for (int64_t x = 0; x < ns; ++x) succ[x] = edges[2 * x];
+  }
   return ns;
 }
 
@@ -294,7 +307,7 @@ static int launch(DevPlan *pl, int p, int q, int nb, int ib, double *A, double *
     attr_set_dev = dev;
   }
   RunArgs a;
-  a.tasks = pl->tasks; a.succ = pl->succ; a.roots = pl->roots; a.nroots = pl->nroots; a.ntask = pl->ntask;
+  a.tasks = pl->tasks; a.succ = reinterpret_cast<const int2 *>(pl->succ); a.roots = pl->roots; a.nroots = pl->nroots; a.ntask = pl->ntask;
   a.cnt = pl->cnt; a.queue = pl->queue; a.ctrl = pl->ctrl; a.epoch = ++pl->epoch;
   for (int l = 0; l <= kLevels; ++l) a.qoff[l] = pl->qoff[l];
   a.A = A; a.T = T; a.C = C;

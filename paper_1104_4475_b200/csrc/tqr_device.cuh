@@ -31,7 +31,7 @@ constexpr int kPanelScratch = 2 * 32 * kTld + 2 * 256 + 8 + 32;
 
 struct RunArgs {
   const DevTask *tasks;
-  const int32_t *succ;          // successor lists (CSR, ranges in the task records)
+  const int2 *succ;             // successor edges (task, its meta) (CSR, ranges in the task records)
   const int32_t *roots;         // tasks without predecessors
   int nroots;
   int ntask;
@@ -1130,8 +1130,8 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
       const int qc = (may_keep && lane < kLevels) ? ld_relaxed(&a.ctrl[kCtrlLevel + 32 * lane]) : 0;
       int mine = -1, mine_lvl = -1;
       for (int x = tk.dep_begin + lane; x < tk.dep_end; x += 32) {
-        const int sc = a.succ[x];
-        const int m = a.tasks[sc].meta;
+        const int2 e = a.succ[x];
+        const int sc = e.x, m = e.y;
         const unsigned need = (unsigned)a.epoch * (unsigned)((m & 0xffff) + ((m >> 20) & 1));
         if (atom_add_acqrel(a.cnt + sc, 1u) + 1u == need) {
           const int lvl = (m >> 16) & 15;
