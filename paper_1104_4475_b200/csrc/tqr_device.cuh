@@ -1112,6 +1112,10 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
     if (t < 0) break;
     __threadfence();
     const DevTask tk = a.tasks[t];
+    // warp 0 issues the loads of its first successor edges now; they land
+    // while the task runs and are consumed only when releasing
+    int2 e0 = make_int2(-1, 0);
+    if (threadIdx.x < 32 && tk.dep_begin + (int)threadIdx.x < tk.dep_end) e0 = __ldg(a.succ + tk.dep_begin + threadIdx.x);
     run_task(a, tk, smem, L, s_resident != 0, mbph);
     __syncthreads();
     prof_mark(PH_STORE);
@@ -1130,7 +1134,7 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
       const int qc = (may_keep && lane < kLevels) ? ld_relaxed(&a.ctrl[kCtrlLevel + 32 * lane]) : 0;
       int mine = -1, mine_lvl = -1;
       for (int x = tk.dep_begin + lane; x < tk.dep_end; x += 32) {
-        const int2 e = a.succ[x];
+        const int2 e = x == tk.dep_begin + lane ? e0 : a.succ[x];
         const int sc = e.x, m = e.y;
         const unsigned need = (unsigned)a.epoch * (unsigned)((m & 0xffff) + ((m >> 20) & 1));
         if (atom_add_acqrel(a.cnt + sc, 1u) + 1u == need) {
