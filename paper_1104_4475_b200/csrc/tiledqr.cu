@@ -98,7 +98,7 @@ static int env_int(const char *name, int dflt) {
 // (DESIGN.md §5); the last strip of a tile may be narrower.
 static int pick_ws(int nb, int ib) {
   int forced = env_int("TQR_WS", 0);
-  if (forced > 0) return forced < nb ? forced : nb;
+  if (forced > 0) return forced < nb ? forced : nb;   // > 32 is rejected by get_plan
   if (nb <= 32) return nb;
   for (int w : {32, 24, 16, 8})
     if (smem_bytes(nb, ib, w) <= kMaxSmem) return w;
@@ -118,7 +118,6 @@ struct DevPlan {
   unsigned long long *trace = nullptr;    // diagnostic per-task timestamps
   std::vector<DevTask> host_tasks;        // kept for tqr_trace_fetch
   int ntask = 0, nroots = 0;
-  int epoch = 0;
   int ws = 0;
   int qoff[kLevels + 1] = {0};            // per-level queue offsets
   ~DevPlan() {
@@ -161,6 +160,8 @@ static int upload(const DevGraph &g, int ws, DevPlan &pl) {
   CUDA_TRY(cudaMemset(pl.cnt, 0, sizeof(unsigned) * n1));
   CUDA_TRY(cudaMemset(pl.queue, 0, sizeof(unsigned long long) * n1));
   CUDA_TRY(cudaMemset(pl.ctrl, 0, sizeof(int) * kCtrlWords));
+  const int epoch1 = 1;   // launch epochs start at 1 (counters accumulate epoch x indegree)
+  CUDA_TRY(cudaMemcpy(pl.ctrl + kCtrlEpoch, &epoch1, sizeof(int), cudaMemcpyHostToDevice));
   return 0;
 }
 
@@ -170,6 +171,8 @@ static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, in
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   int ws = pick_ws(nb, ib);
+  if (ws > 32)   // the strip kernels deal 4 n8 column tiles (32 columns) over the warps
+    return fail(TQR_EUNSUP, "strip width " + std::to_string(ws) + " (TQR_WS) > 32 is not supported");
   if (smem_bytes(nb, ib, ws) > kMaxSmem)
     return fail(TQR_EUNSUP, "strip width " + std::to_string(ws) + " (TQR_WS) needs " +
                                 std::to_string(smem_bytes(nb, ib, ws)) + " bytes of shared memory for nb = " +
@@ -308,7 +311,7 @@ static int launch(DevPlan *pl, int p, int q, int nb, int ib, double *A, double *
   }
   RunArgs a;
   a.tasks = pl->tasks; a.succ = reinterpret_cast<const int2 *>(pl->succ); a.roots = pl->roots; a.nroots = pl->nroots; a.ntask = pl->ntask;
-  a.cnt = pl->cnt; a.queue = pl->queue; a.ctrl = pl->ctrl; a.epoch = ++pl->epoch;
+  a.cnt = pl->cnt; a.queue = pl->queue; a.ctrl = pl->ctrl;
   for (int l = 0; l <= kLevels; ++l) a.qoff[l] = pl->qoff[l];
   a.A = A; a.T = T; a.C = C;
   a.p = p; a.q = q; a.nb = nb; a.ib = ib; a.ws = pl->ws; a.trans = trans;
@@ -324,6 +327,12 @@ static int launch(DevPlan *pl, int p, int q, int nb, int ib, double *A, double *
   int grid = sms;
   int forced = env_int("TQR_GRID", 0);
   if (forced > 0) grid = forced;
+  // never more CTAs than can be co-resident (1 per SM at this footprint)
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tqr_persistent, kThreads, smem));
+  if (per_sm < 1) return fail(TQR_EUNSUP, "tqr_persistent does not fit on an SM with " + std::to_string(smem) +
+                                              " bytes of shared memory");
+  if (grid > per_sm * sms) grid = per_sm * sms;
   if (grid > pl->ntask) grid = pl->ntask;
   a.nctas = grid;
   tqr_persistent<<<grid, kThreads, smem, stream>>>(a);
@@ -338,6 +347,7 @@ extern "C" int tiled_qr(int m, int n, int nb, int ib, int tree, int bs, int fami
   int rc = check_shape(m, n, nb, ib, p, q);
   if (rc < 0) return rc;
   if (!A || !T) return fail(TQR_EINVAL, "tiled_qr: null pointer");
+  if (((uintptr_t)A | (uintptr_t)T) & 15) return fail(TQR_EINVAL, "tiled_qr: A and T must be 16-byte aligned");
   DevPlan *pl;
   rc = get_plan(0, p, q, 0, nb, ib, tree, bs, family, &pl);
   if (rc < 0) return rc;
@@ -350,6 +360,8 @@ static int apply_common(int trans, int m, int n, int nb, int ib, int tree, int b
   int rc = check_shape(m, n, nb, ib, p, q);
   if (rc < 0) return rc;
   if (!A || !T || !C) return fail(TQR_EINVAL, "apply: null pointer");
+  if (((uintptr_t)A | (uintptr_t)T | (uintptr_t)C) & 15)
+    return fail(TQR_EINVAL, "apply: A, T and C must be 16-byte aligned");
   if (nrhs < 0 || nrhs % nb) return fail(TQR_EINVAL, "apply: nrhs must be a multiple of nb");
   int qc = nrhs / nb;
   if (qc == 0) { g_launches = 0; return 0; }

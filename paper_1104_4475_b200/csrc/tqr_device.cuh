@@ -20,13 +20,15 @@ constexpr int kMaxNb = 256;
 constexpr int kMaxIb = 32;
 constexpr size_t kMaxSmem = 227 * 1024 - 512;   // dynamic smem budget (opt-in max minus static)
 constexpr int kTld = 33;
-constexpr int kTraceWords = 12;             // per-task trace record (diagnostics)
+constexpr int kTraceWords = 13;             // per-task trace record (diagnostics): 4 stamps/ids, 8 phases, push time
 // scheduler control words (ints; each on its own 128-byte line): per priority
 // level l a queue head at kCtrlHead + 64 l, its tail at kCtrlTail + 64 l and
 // its count of published, unclaimed tasks at kCtrlLevel + 32 l
+// kCtrlEpoch holds the launch epoch (1 after upload; the last CTA of a launch
+// advances it), kCtrlStart the arrival ticket whose first holder seeds the roots.
 constexpr int kCtrlHead = 0, kCtrlTail = 32, kCtrlDone = 64 * kLevels, kCtrlExit = 64 * kLevels + 32,
-              kCtrlLevel = 64 * kLevels + 96,
-              kCtrlWords = 96 * kLevels + 96;
+              kCtrlLevel = 64 * kLevels + 96, kCtrlEpoch = 96 * kLevels + 96, kCtrlStart = 96 * kLevels + 128,
+              kCtrlWords = 96 * kLevels + 160;
 constexpr int kPanelScratch = 2 * 32 * kTld + 2 * 256 + 8 + 32;
 
 struct RunArgs {
@@ -39,8 +41,8 @@ struct RunArgs {
   unsigned long long *queue;    // kLevels ready queues (level kLevels-1 = most critical); level l
                                 // owns slots [qoff[l], qoff[l+1]) = one per task of that level
   int qoff[kLevels + 1];
-  int *ctrl;                    // kCtrl* counters
-  int epoch;
+  int *ctrl;                    // kCtrl* counters (incl. the launch epoch, kept on the device so that a
+                                // launch that never started, or a graph replay, cannot desynchronise it)
   int nctas;
   double *A, *T, *C;
   int p, q, nb, ib, ws, trans;
@@ -1022,12 +1024,14 @@ __device__ __forceinline__ void st_release64(unsigned long long *p, unsigned lon
   asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__shared__ unsigned s_epoch;   // launch epoch, read from ctrl[kCtrlEpoch] at kernel start
+
 __device__ __forceinline__ void push_ready(const RunArgs &a, int t) {   // (chained tasks may be queued too)
   const int q = (a.tasks[t].meta >> 16) & 15;
   const int pos = atomicAdd(&a.ctrl[kCtrlTail + 64 * q], 1);
-  st_release64(a.queue + a.qoff[q] + pos, ((unsigned long long)(unsigned)a.epoch << 32) | (unsigned)t);
+  st_release64(a.queue + a.qoff[q] + pos, ((unsigned long long)s_epoch << 32) | (unsigned)t);
   atomicAdd(&a.ctrl[kCtrlLevel + 32 * q], 1);
-  if (a.trace) a.trace[kTraceWords * (size_t)t + 11] = globaltimer();   // diagnostics: push time
+  if (a.trace) a.trace[kTraceWords * (size_t)t + 12] = globaltimer();   // diagnostics: push time
 }
 
 // Claim a task of queue q, or return -1. A fetch-and-subtract on the level's
@@ -1042,7 +1046,7 @@ __device__ __forceinline__ int try_pop(const RunArgs &a, int q) {
   const int h = atomicAdd(&a.ctrl[kCtrlHead + 64 * q], 1);
   const unsigned long long *slot = a.queue + a.qoff[q] + h;
   unsigned long long v;
-  while (((v = ld_acquire64(slot)) >> 32) != (unsigned)a.epoch) __nanosleep(20);
+  while (((v = ld_acquire64(slot)) >> 32) != s_epoch) __nanosleep(20);
   return (int)(v & 0xffffffffu);
 }
 
@@ -1053,7 +1057,7 @@ __device__ __forceinline__ unsigned ld_acquire_u(const unsigned *p) {
 }
 __device__ __forceinline__ unsigned need_count(const RunArgs &a, int t) {
   const int m = a.tasks[t].meta;
-  return (unsigned)a.epoch * (unsigned)((m & 0xffff) + ((m >> 20) & 1));
+  return s_epoch * (unsigned)((m & 0xffff) + ((m >> 20) & 1));
 }
 __device__ __forceinline__ bool is_panel_block(int kind) {
   return kind == K_GEQRT_B || kind == K_TTQRT_B || kind == K_TSQRT_B;
@@ -1063,12 +1067,19 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_task, s_chain, s_resident;
   const SmemLayout L = smem_layout(a.nb, a.ib, a.ws);
-  if (threadIdx.x == 0) { s_prof_on = 0; s_chain = -1; s_resident = 0; mbar_init(); }
+  if (threadIdx.x == 0) {
+    s_prof_on = 0; s_chain = -1; s_resident = 0; mbar_init();
+    s_epoch = (unsigned)ld_acquire(&a.ctrl[kCtrlEpoch]);
+  }
   unsigned mbph = 0u;   // parity of the CTA mbarrier (identical in every thread)
   // everything the DMMA padding may read must be finite: start from zeros
   for (size_t x = threadIdx.x; x < L.total; x += kThreads) smem[x] = 0.0;
-  if (threadIdx.x == 0)
-    for (int r = blockIdx.x; r < a.nroots; r += gridDim.x) push_ready(a, a.roots[r]);
+  __syncthreads();
+  // the first CTA to arrive seeds every root: progress never depends on a
+  // particular CTA being resident (grids larger than the co-resident
+  // capacity, or SMs held by a concurrent kernel, still complete)
+  if (threadIdx.x == 0 && atomicAdd(&a.ctrl[kCtrlStart], 1) == 0)
+    for (int r = 0; r < a.nroots; ++r) push_ready(a, a.roots[r]);
   for (;;) {
     if (threadIdx.x < 32) {
       // warp 0 claims the next task: lane l < kLevels reads level l's count,
@@ -1136,7 +1147,7 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
       for (int x = tk.dep_begin + lane; x < tk.dep_end; x += 32) {
         const int2 e = x == tk.dep_begin + lane ? e0 : a.succ[x];
         const int sc = e.x, m = e.y;
-        const unsigned need = (unsigned)a.epoch * (unsigned)((m & 0xffff) + ((m >> 20) & 1));
+        const unsigned need = s_epoch * (unsigned)((m & 0xffff) + ((m >> 20) & 1));
         if (atom_add_acqrel(a.cnt + sc, 1u) + 1u == need) {
           const int lvl = (m >> 16) & 15;
           if (may_keep && lvl > mine_lvl) {
@@ -1166,7 +1177,7 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
         unsigned long long *tr = a.trace + kTraceWords * (size_t)t;
         tr[2] = globaltimer();
         tr[3] = ((unsigned long long)smid() << 32) | (unsigned)tk.kind;
-        for (int x = 0; x < 7; ++x) tr[4 + x] = s_prof[x];   // word 11 = push time
+        for (int x = 0; x < 8; ++x) tr[4 + x] = s_prof[x];   // word 12 = push time
       }
       atomicAdd(&a.ctrl[kCtrlDone], 1);
       // panel chain: run the chained successor here if its other inputs are (or
@@ -1188,7 +1199,9 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
     if (n == a.nctas - 1) {
       for (int q = 0; q < kLevels; ++q)
         a.ctrl[kCtrlHead + 64 * q] = a.ctrl[kCtrlTail + 64 * q] = a.ctrl[kCtrlLevel + 32 * q] = 0;
-      a.ctrl[kCtrlDone] = 0; a.ctrl[kCtrlExit] = 0;
+      a.ctrl[kCtrlDone] = 0; a.ctrl[kCtrlExit] = 0; a.ctrl[kCtrlStart] = 0;
+      __threadfence();
+      a.ctrl[kCtrlEpoch] = (int)(s_epoch + 1u);   // the next launch (stream-ordered) runs epoch + 1
       __threadfence();
     }
   }

@@ -17,14 +17,20 @@ def test_table4b_asap_15x3(golden_matrix):
 
 def test_table4c_grasap1_15x3(golden_matrix):
     """Table 4(c) Grasap(1): 'Grasap(1) finishes at time-step 62, while Greedy
-    finishes at time-step 64' (line 691). Of the 39 printed times, (7,3) = 56 is
-    not reproduced (52 here); reading R11 pins this discrepancy."""
+    finishes at time-step 64' (line 691); 38 of the 39 printed zeroing times
+    agree. Tile (7,3) is checked against the printed value in the xfail test below."""
     g = golden_matrix("table4_grasap1_15x3.csv")
     z = asap.zero_times(15, 3, 1)
-    diff = {k for k in g if z[k] != g[k]}
-    assert diff == {(7, 3)} and z[(7, 3)] == 52 and g[(7, 3)] == 56
+    assert {k: z[k] for k in g if k != (7, 3)} == {k: v for k, v in g.items() if k != (7, 3)}
     assert asap.critical_path(15, 3, 1) == 62
     assert asap.critical_path(15, 3, 0) == 64
+
+
+@pytest.mark.xfail(strict=True, reason="DESIGN.md reading R11: the tiled ASAP reading gives 52 for tile (7,3) "
+                                        "of Table 4(c); the printed value is 56")
+def test_table4c_grasap1_tile_7_3_printed(golden_matrix):
+    g = golden_matrix("table4_grasap1_15x3.csv")
+    assert asap.zero_times(15, 3, 1)[(7, 3)] == g[(7, 3)] == 56
 
 
 def test_grasap0_is_greedy_and_lists_valid():
@@ -56,9 +62,15 @@ def test_table5b_asap(golden_rows):
 
 
 @pytest.mark.slow
-def test_table5b_asap_128():
+def test_table5b_asap_128_128():
     assert asap.critical_path(128, 128, 128) == 2756
-    assert asap.critical_path(128, 64, 64) == 1734      # printed: 1748
+
+
+@pytest.mark.slow
+@pytest.mark.xfail(strict=True, reason="DESIGN.md reading R11: the tiled ASAP reading gives 1734 for 128 x 64; "
+                                        "Table 5(b) prints 1748")
+def test_table5b_asap_128_64_printed():
+    assert asap.critical_path(128, 64, 64) == 1748
 
 
 @pytest.mark.parametrize("tree", ["asap", "grasap"])
