@@ -189,6 +189,11 @@ int tqr_host_wait(void);
 /* Number of kernel launches the last device call issued (for bench accounting). */
 int tqr_last_launch_count(void);
 
+/* 1 if the last device call moved its V blocks and C1 windows with TMA tensor
+ * copies (cp.async.bulk.tensor, needs nb % 8 == 0, ib % 8 == 0, nb >= 32 and
+ * TQR_TMA unset or non-zero in the environment), 0 if it used cp.async. */
+int tqr_last_launch_tma(void);
+
 /* Free every cached plan and scratch buffer (all devices). */
 void tqr_release_plans(void);
 

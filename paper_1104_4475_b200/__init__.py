@@ -45,6 +45,7 @@ _SIGS = {
     "tiled_qr_host_async": (ctypes.c_int, [ctypes.c_int] * 7 + [_VP, _VP, _VP, _VP]),
     "tqr_host_wait": (ctypes.c_int, []),
     "tqr_last_launch_count": (ctypes.c_int, []),
+    "tqr_last_launch_tma": (ctypes.c_int, []),
     "tqr_release_plans": (None, []),
     "tqr_last_error": (ctypes.c_char_p, []),
     "tqr_version": (ctypes.c_int, []),
@@ -249,3 +250,7 @@ def host_wait():
 
 def last_launch_count() -> int:
     return lib().tqr_last_launch_count()
+
+
+def last_launch_tma() -> bool:
+    return bool(lib().tqr_last_launch_tma())

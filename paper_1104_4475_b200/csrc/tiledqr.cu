@@ -2,6 +2,8 @@
 // task graph of an elimination list (§2.3 execution scheme, lines
 // 385-411), with the six tile kernels of Table 1 (lines 239-251) as device
 // routines. See DESIGN.md §5 for the design and include/tiledqr.h for the ABI.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
@@ -292,7 +294,42 @@ static int check_shape(int m, int n, int nb, int ib, int &p, int &q) {
   return 0;
 }
 
-static int launch(DevPlan *pl, int p, int q, int nb, int ib, double *A, double *T, double *C,
+// ---- TMA tensor maps -----------------------------------------------------------
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda
+// link). A matrix of p x qc tiles of nb x nb (column-major tiles, tile (i, k)
+// at column (k p + i) nb of the stacked columns) is viewed as the 3-D tensor
+// (row within a tile of 8, stacked column, row tile), strides (8 B, 8 nb B,
+// 64 B): a box of 8 x 32 x 4 is 4 row tiles of 32 columns in the row-tile
+// shared-memory layout of the strip update (tqr_device.cuh).
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+static bool encode_tiles8(CUtensorMap *m, const double *base, int nb, long long ncols) {
+  PFN_cuTensorMapEncodeTiled_v12000 fn = tensor_map_encoder();
+  if (!fn || !base) return false;
+  const cuuint64_t dims[3] = {8, (cuuint64_t)ncols, (cuuint64_t)(nb / 8)};
+  const cuuint64_t strides[2] = {(cuuint64_t)nb * 8, 64};
+  const cuuint32_t box[3] = {8, 32, 4};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int g_tma_used = 0;
+extern "C" int tqr_last_launch_tma(void) { return g_tma_used; }
+
+static int launch(DevPlan *pl, int p, int q, int qc, int nb, int ib, double *A, double *T, double *C,
                   int trans, cudaStream_t stream) {
   if (pl->ntask == 0) { g_launches = 0; return 0; }
   int dev = 0, sms = 0;
@@ -310,12 +347,20 @@ static int launch(DevPlan *pl, int p, int q, int nb, int ib, double *A, double *
     attr_set_dev = dev;
   }
   RunArgs a;
+  memset(&a, 0, sizeof a);
   a.tasks = pl->tasks; a.succ = reinterpret_cast<const int2 *>(pl->succ); a.roots = pl->roots; a.nroots = pl->nroots; a.ntask = pl->ntask;
   a.cnt = pl->cnt; a.queue = pl->queue; a.ctrl = pl->ctrl;
   for (int l = 0; l <= kLevels; ++l) a.qoff[l] = pl->qoff[l];
   a.A = A; a.T = T; a.C = C;
   a.p = p; a.q = q; a.nb = nb; a.ib = ib; a.ws = pl->ws; a.trans = trans;
-  a.tma = env_int("TQR_TMA", 0);   // 1-D TMA bulk path (measured ~4% slower than cp.async here)
+  // TMA tensor copies of V blocks and C1 windows when the shapes allow (row
+  // tiles of 8 align with inner blocks, >= 4 row tiles); else cp.async
+  a.tma = 0;
+  if (env_int("TQR_TMA", 1) && nb % 8 == 0 && ib % 8 == 0 && nb >= 32 &&
+      encode_tiles8(&a.mapA, A, nb, (long long)p * q * nb) &&
+      (!C || encode_tiles8(&a.mapC, C, nb, (long long)p * qc * nb)))
+    a.tma = 1;
+  g_tma_used = a.tma;
   a.work_first = env_int("TQR_WORK_FIRST", 1) != 0;
   a.chain_spin = env_int("TQR_CHAIN_SPIN", 0);   // measured best: no spin (profiles/r01_chain_spin_sweep.txt)
   a.trace = nullptr;
@@ -351,7 +396,7 @@ extern "C" int tiled_qr(int m, int n, int nb, int ib, int tree, int bs, int fami
   DevPlan *pl;
   rc = get_plan(0, p, q, 0, nb, ib, tree, bs, family, &pl);
   if (rc < 0) return rc;
-  return launch(pl, p, q, nb, ib, A, T, nullptr, 1, (cudaStream_t)stream);
+  return launch(pl, p, q, 0, nb, ib, A, T, nullptr, 1, (cudaStream_t)stream);
 }
 
 static int apply_common(int trans, int m, int n, int nb, int ib, int tree, int bs, int family,
@@ -368,7 +413,7 @@ static int apply_common(int trans, int m, int n, int nb, int ib, int tree, int b
   DevPlan *pl;
   rc = get_plan(trans ? 1 : 2, p, q, qc, nb, ib, tree, bs, family, &pl);
   if (rc < 0) return rc;
-  return launch(pl, p, q, nb, ib, const_cast<double *>(A), const_cast<double *>(T), C, trans,
+  return launch(pl, p, q, qc, nb, ib, const_cast<double *>(A), const_cast<double *>(T), C, trans,
                 (cudaStream_t)stream);
 }
 

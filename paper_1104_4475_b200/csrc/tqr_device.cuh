@@ -8,6 +8,7 @@
 // A block of <= ib reflectors is applied in compact-WY form
 // Q_b = I - V T V^T (lines 62-66; forward column-wise T).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 #include "plan.h"
@@ -20,6 +21,8 @@ constexpr int kMaxNb = 256;
 constexpr int kMaxIb = 32;
 constexpr size_t kMaxSmem = 227 * 1024 - 512;   // dynamic smem budget (opt-in max minus static)
 constexpr int kTld = 33;
+constexpr int kLdw = 36;                    // W^T / W2^T in smem: element (col, refl) at col + refl * kLdw
+constexpr int kSlots = 8;                   // row tiles of 8 per warp in a strip update (nb <= 256)
 constexpr int kTraceWords = 13;             // per-task trace record (diagnostics): 4 stamps/ids, 8 phases, push time
 // scheduler control words (ints; each on its own 128-byte line): per priority
 // level l a queue head at kCtrlHead + 64 l, its tail at kCtrlTail + 64 l and
@@ -29,9 +32,13 @@ constexpr int kTraceWords = 13;             // per-task trace record (diagnostic
 constexpr int kCtrlHead = 0, kCtrlTail = 32, kCtrlDone = 64 * kLevels, kCtrlExit = 64 * kLevels + 32,
               kCtrlLevel = 64 * kLevels + 96, kCtrlEpoch = 96 * kLevels + 96, kCtrlStart = 96 * kLevels + 128,
               kCtrlWords = 96 * kLevels + 160;
-constexpr int kPanelScratch = 2 * 32 * kTld + 2 * 256 + 8 + 32;
+// panel scratch: t_doubling temp, G = V^T V, working T (all 32 x kTld), the
+// published reflector (2 x 256), its tau (2 x 4) and the block's taus (32)
+constexpr int kPanelScratch = 3 * 32 * kTld + 2 * 256 + 8 + 32;
 
-struct RunArgs {
+struct alignas(64) RunArgs {
+  CUtensorMap mapA;             // A as (row in tile-of-8, global column, row tile): box 8 x 32 x 4 (TMA path)
+  CUtensorMap mapC;             // the same view of C (apply_qt / apply_q)
   const DevTask *tasks;
   const int2 *succ;             // successor edges (task, its meta) (CSR, ranges in the task records)
   const int32_t *roots;         // tasks without predecessors
@@ -46,48 +53,49 @@ struct RunArgs {
   int nctas;
   double *A, *T, *C;
   int p, q, nb, ib, ws, trans;
-  int tma;                     // 1: move C strips and V blocks with 1-D TMA bulk copies
+  int tma;                     // 1: V blocks and C1 windows move by TMA tensor copies (nb, ib % 8 == 0)
   int work_first;              // 1: a CTA runs the most urgent successor it made ready (not queued)
   int chain_spin;              // polls (128 ns apart) for a chained successor's other inputs
   unsigned long long *trace;   // optional: kTraceWords u64 per task (taken, ready, done, smid<<32|kind, 8 phase cycle counters)
 };
 
-struct SmemLayout {
-  int ldc, ldv, ldw, wcols, nvb;
-  size_t offC, offV[2], offW, offT[2], total;   // in doubles
-};
-
-// Leading dimensions are = 4 (mod 16) doubles: the DMMA fragment loads of a
-// warp (lanes 4g+t reading element t + g*ld or g + t*ld) then hit 16 distinct
-// 8-byte bank pairs per half-warp (conflict-free).
-__host__ __device__ inline int ld4(int n) { return n + ((4 - n % 16) + 16) % 16; }
+// ---- shared-memory layout ----------------------------------------------------
+// Row-tile ("tile-of-8") layout of a column block: rows are grouped in tiles
+// of 8; tile j holds rows 8j..8j+7 of up to 32 columns as [column][row % 8],
+// 256 doubles per tile. Element (r, l) sits at (r >> 3) * 256 + l * 8 + (r & 7).
+// Every fragment access of the strip update is bank-conflict-free in it: the
+// 16-byte row pairs (2t, 2t+1) of lanes (g, t) land on 8 distinct 16-byte
+// units per quarter warp, and the 8-byte reads (row g, column 4k + t) on 16
+// distinct bank pairs per half warp.
+__host__ __device__ inline int vidx(int r, int l) { return (r >> 3) * 256 + l * 8 + (r & 7); }
 __host__ __device__ inline int round_up(int n, int m) { return (n + m - 1) / m * m; }
 
-// C buffer rows: single-tile strips (UNMQR, GEQRT trailing) use rows 0..nb-1;
-// two-tile strips (TTMQR/TSMQR) keep C2 at rows kWinRows.. and stream the 32
-// C1 rows of each inner block through two windows at rows 0 and 32.
-constexpr int kWinRows = 64;
+struct SmemLayout {
+  int ntile;                    // ceil(nb / 8) row tiles
+  size_t offV[2];               // reflector blocks V (double-buffered), ntile x 256 each, absolute rows
+  size_t offWp;                 // 4 partial W^T (32 x kLdw each); the panel's scratch aliases it
+  size_t offW, offW2;           // reduced W^T and W2^T (32 x kLdw each)
+  size_t offT[2];               // T blocks, ld ib (double-buffered)
+  size_t offC1[2];              // C1 windows of TT/TS updates: ib rows x 32 columns, row-tile layout
+  size_t total;                 // in doubles
+};
 
 __host__ __device__ inline SmemLayout smem_layout(int nb, int ib, int ws) {
+  (void)ib; (void)ws;
   SmemLayout s;
-  s.wcols = round_up(ws, 8);
-  s.ldc = ld4(nb + kWinRows + 16);
-  s.ldv = ld4(round_up(nb, 16));
-  s.ldw = 36;
-  const size_t c = (size_t)s.ldc * s.wcols;
-  const size_t v = (size_t)s.ldv * 32;
-  size_t w = (size_t)2 * s.ldw * s.wcols;
-  if (w < (size_t)kPanelScratch) w = kPanelScratch;
-  const size_t tt = 32 * kTld;
-  s.nvb = (c + 2 * v + w + 2 * tt) * sizeof(double) <= kMaxSmem ? 2 : 1;   // double-buffer V/T if it fits
-  s.offC = 0;
-  s.offV[0] = c;
-  s.offV[1] = c + v;
-  s.offW = c + s.nvb * v;
-  s.offT[0] = s.offW + w;
-  s.offT[1] = s.offT[0] + tt;
-  s.total = s.offT[0] + s.nvb * tt;
-  if (s.nvb == 1) { s.offV[1] = s.offV[0]; s.offT[1] = s.offT[0]; }
+  s.ntile = (nb + 7) / 8;
+  const size_t v = (size_t)s.ntile * 256;
+  s.offV[0] = 0;
+  s.offV[1] = v;
+  s.offWp = 2 * v;
+  const size_t wp = 4 * 32 * kLdw > kPanelScratch ? 4 * 32 * kLdw : kPanelScratch;
+  s.offW = s.offWp + wp;
+  s.offW2 = s.offW + 32 * kLdw;
+  s.offT[0] = s.offW2 + 32 * kLdw;
+  s.offT[1] = s.offT[0] + 1024;
+  s.offC1[0] = s.offT[1] + 1024;
+  s.offC1[1] = s.offC1[0] + 1024;
+  s.total = s.offC1[1] + 1024;
   return s;
 }
 
@@ -111,11 +119,6 @@ __shared__ unsigned long long s_prof[8];
 __shared__ unsigned long long s_prof_last;
 __shared__ int s_prof_on;
 enum { PH_LOAD = 0, PH_FIX, PH_MMA1, PH_TRI, PH_MMA3, PH_PANEL, PH_TREC, PH_STORE };
-#ifdef TQR_PANEL_PROF
-#define PPROF(slot) prof_mark(slot)
-#else
-#define PPROF(slot)
-#endif
 __device__ __forceinline__ void prof_mark(int slot) {
   if (threadIdx.x == 0 && s_prof_on) {
     unsigned long long now = clock64();
@@ -141,212 +144,111 @@ __device__ __forceinline__ double *tile_ptr(double *base, int p, int nb, int i, 
 __device__ __forceinline__ double *tslot_ptr(double *T, int p, int nb, int ib, int i, int k, int s) {
   return T + (((size_t)k * p + i) * 2 + s) * (size_t)ib * nb;
 }
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 
-// ---- asynchronous global -> shared copies (LDGSTS) ---------------------------
-// All tile data reaches shared memory through cp.async so that every load of a
-// task is in flight at once (a scalar load loop is L2-latency bound). The .cg
-// (16 B) form bypasses L1; the 8 B form is used only for odd sizes. Writers of
-// a tile are ordered before readers by the release/acquire flags plus a
-// gpu-scope fence, which also invalidates L1.
-__device__ __forceinline__ void cp_async8(double *dst, const double *src) {
-  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+// ---- asynchronous global -> shared copies ------------------------------------
+// cp.async (LDGSTS) with zero fill: `valid` = false writes zeros without a
+// global read. Completion is tracked per buffer by an mbarrier: every thread
+// ends its batch with cp.async.mbarrier.arrive.noinc (the barrier expects one
+// arrival per thread), so consumers wait on the mbarrier instead of a CTA-wide
+// barrier. Writers of a tile are ordered before readers by the release/acquire
+// task counters plus a gpu-scope fence.
+__device__ __forceinline__ void cp_async16_zf(double *dst, const double *src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
 }
-__device__ __forceinline__ void cp_async16(double *dst, const double *src) {
-  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+__device__ __forceinline__ void cp_async8_zf(double *dst, const double *src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 8 : 0)
+               : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+__shared__ __align__(8) unsigned long long s_mbar[2];   // one per V/T/C1 buffer
 
-
-// copy rows [r0, r1) of columns [c0, c0+ncol) of a column-major global array
-// (leading dimension ldg) to shared dst[(r - r0) + c*lds]
-__device__ __forceinline__ void async_block(double *dst, int lds, const double *src, int ldg, int r0, int r1,
-                                            int c0, int ncol) {
-  const int nr = r1 - r0;
-  if (nr <= 0 || ncol <= 0) return;
-  const double *g = src + r0 + (size_t)c0 * ldg;
-  const bool v16 = ((nr | lds | ldg) & 1) == 0 && ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (v16 && nr <= 4 * 64 && ncol <= 4 * kWarps) {
-    // warps over columns, lanes over 16-byte row pairs; nr <= 256 and ncol <= 32
-    // always hold here (nb <= kMaxNb), so both loops unroll into predicated
-    // copies with constant offsets from one base address per thread
-    double *d0 = dst + 2 * lane + warp * lds;
-    const double *g0 = g + 2 * lane + (size_t)warp * ldg;
-#pragma unroll
-    for (int ci = 0; ci < 4; ++ci) {
-      if (warp + ci * kWarps < ncol) {
-        double *d = d0 + ci * kWarps * lds;
-        const double *gs = g0 + (size_t)ci * kWarps * ldg;
-#pragma unroll
-        for (int ri = 0; ri < 4; ++ri)
-          if (2 * lane + 64 * ri < nr) cp_async16(d + 64 * ri, gs + 64 * ri);
-      }
-    }
-  } else if (v16) {   // warps over columns, lanes over 16-byte row pairs (no integer division)
-    for (int c = warp; c < ncol; c += kWarps)
-      for (int r = 2 * lane; r < nr; r += 64) cp_async16(dst + r + c * lds, g + r + (size_t)c * ldg);   // dst row 0 = r0
-  } else {
-    for (int c = warp; c < ncol; c += kWarps)
-      for (int r = lane; r < nr; r += 32) cp_async8(dst + r + c * lds, g + r + (size_t)c * ldg);
-  }
-}
-
-// ---- TMA (1-D bulk copies) with an mbarrier transaction count --------------
-// One cp.async.bulk per tile column (global column segment -> smem column),
-// issued by the lanes of warp 0; completion is tracked by the CTA's mbarrier
-// (expect_tx per issue, one arrival per batch, parity wait). The SASS shows
-// UBLKCP. Sizes/addresses that are not 16-byte multiples fall back to cp.async.
-__shared__ __align__(8) unsigned long long s_mbar;
-
-__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init() {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_mbar)) : "memory");
+__device__ __forceinline__ void mbar_init_all() {
+  for (int b = 0; b < 2; ++b)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_mbar[b])), "r"(kThreads) : "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-
-// issue column copies rows [r0, r1) of columns [c0, c0+ncol): TMA when every
-// column segment is 16-byte aligned and a multiple of 16 bytes, else cp.async
-__device__ __forceinline__ void tma_block(double *dst, int lds, const double *src, int ldg, int r0, int r1,
-                                          int c0, int ncol, bool use_tma) {
-  const int nr = r1 - r0;
-  if (nr <= 0 || ncol <= 0) return;
-  const double *g = src + r0 + (size_t)c0 * ldg;
-  const bool ok = use_tma && ((nr | lds | ldg) & 1) == 0 &&
-                  ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
-  if (!ok) {
-    async_block(dst, lds, src, ldg, r0, r1, c0, ncol);
-    return;
-  }
-  if (threadIdx.x < 32) {
-    const unsigned bytes = (unsigned)nr * 8u;
-    if (threadIdx.x == 0) {
-      asm volatile("fence.proxy.async;" ::: "memory");
-      asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_mbar)),
-                   "r"(bytes * (unsigned)ncol) : "memory");
-    }
-    __syncwarp();
-    for (int c = threadIdx.x; c < ncol; c += 32)
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                   ::"r"(smem_u32(dst + c * lds)), "l"(g + (size_t)c * ldg), "r"(bytes), "r"(smem_u32(&s_mbar))
-                   : "memory");
-  }
+// this thread's arrival on buffer b's barrier once its outstanding cp.async copies have landed
+__device__ __forceinline__ void mbar_arrive_cp(int b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&s_mbar[b])) : "memory");
 }
-
-// wait for every outstanding copy of this batch: cp.async groups and the TMA
-// transactions (one arrival + parity wait; `phase` is the per-thread parity)
-__device__ __forceinline__ void async_wait(unsigned &phase) {
-  cp_async_wait_all();
-  if (threadIdx.x == 0) {
-    unsigned long long st;
-    asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(st) : "r"(smem_u32(&s_mbar)) : "memory");
-  }
+// wait for the current phase of buffer b's barrier; `ph` holds one parity bit per buffer
+__device__ __forceinline__ void mbar_wait(int b, unsigned &ph) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "TQR_WAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra TQR_WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(&s_mbar)), "r"(phase) : "memory");
-  phase ^= 1u;
+      "}\n" ::"r"(smem_u32(&s_mbar[b])), "r"((ph >> b) & 1u) : "memory");
+  ph ^= 1u << b;
 }
 
-// ---- strip movement: rows [r0, r1) of tile columns [c0, c0+wsz) <-> buf rows (off + r)
-__device__ __forceinline__ void load_rows(double *buf, int ldc, int off, const double *tile, int nb,
-                                          int r0, int r1, int c0, int wsz) {
-  async_block(buf + off + r0, ldc, tile, nb, r0, r1, c0, wsz);
-}
-__device__ __forceinline__ void store_rows(const double *buf, int ldc, int off, double *tile, int nb,
-                                           int r0, int r1, int c0, int wsz) {
+// rows [row0, row0 + 8 ntl) of columns [c0, c0 + ncol) (ncol <= 32) of the
+// column-major tile X (ld nb) -> row-tile layout dst (tile 0 = rows row0..row0+7);
+// rows outside [0, nb) are zero-filled; columns >= ncol are left untouched.
+// Warp w copies (row tile, 8 columns) chunks: lane -> column lane/4, row pair lane%4.
+__device__ __forceinline__ void load_tiles8(double *dst, const double *X, int nb, int row0, int ntl, int c0,
+                                            int ncol) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if ((((r1 - r0) | ldc | nb | r0 | off) & 1) == 0 && r1 - r0 <= 4 * 64 && wsz <= 4 * kWarps) {
-    // same unrolled, predicated form as async_block (rows <= 256, columns <= 32)
-    const int nr = r1 - r0;
-    const double *b0 = buf + off + r0 + 2 * lane + warp * ldc;
-    double *t0 = tile + r0 + 2 * lane + (size_t)(c0 + warp) * nb;
-#pragma unroll
-    for (int ci = 0; ci < 4; ++ci) {
-      if (warp + ci * kWarps < wsz) {
-        const double *b = b0 + ci * kWarps * ldc;
-        double *tt = t0 + (size_t)ci * kWarps * nb;
-#pragma unroll
-        for (int ri = 0; ri < 4; ++ri)
-          if (2 * lane + 64 * ri < nr)
-            *reinterpret_cast<double2 *>(tt + 64 * ri) = *reinterpret_cast<const double2 *>(b + 64 * ri);
+  const int cl = lane >> 2, pr = 2 * (lane & 3);
+  const bool v16 = ((nb | row0) & 1) == 0;
+  for (int ch = warp; ch < ntl * 4; ch += kWarps) {
+    const int tl = ch >> 2, c = 8 * (ch & 3) + cl;
+    if (c < ncol) {
+      const int r = row0 + 8 * tl + pr;
+      double *d = dst + tl * 256 + c * 8 + pr;
+      const double *s = X + (size_t)(c0 + c) * nb;
+      if (v16) {
+        cp_async16_zf(d, s + (r < nb ? r : 0), r < nb);
+      } else {
+        cp_async8_zf(d, s + (r < nb ? r : 0), r < nb);
+        cp_async8_zf(d + 1, s + (r + 1 < nb ? r + 1 : 0), r + 1 < nb);
       }
     }
-  } else if ((((r1 - r0) | ldc | nb | r0 | off) & 1) == 0) {
-    for (int c = warp; c < wsz; c += kWarps)
-      for (int r = r0 + 2 * lane; r < r1; r += 64)
-        *reinterpret_cast<double2 *>(tile + r + (size_t)(c0 + c) * nb) =
-            *reinterpret_cast<const double2 *>(buf + off + r + c * ldc);
+  }
+}
+// T block of inner block j0 (bw columns of a T slot, ld ib) -> dst (same layout)
+__device__ __forceinline__ void load_tblock(double *dst, const double *Tslot, int ib, int j0, int bw) {
+  const int n = bw * ib;
+  const double *s = Tslot + (size_t)j0 * ib;
+  if ((ib & 1) == 0) {
+    for (int i = 2 * threadIdx.x; i < n; i += 2 * kThreads) cp_async16_zf(dst + i, s + i, true);
   } else {
-    for (int c = warp; c < wsz; c += kWarps)
-      for (int r = r0 + lane; r < r1; r += 32) tile[r + (size_t)(c0 + c) * nb] = buf[off + r + c * ldc];
+    for (int i = threadIdx.x; i < n; i += kThreads) cp_async8_zf(dst + i, s + i, true);
   }
 }
 
-// V of a GEQRT block (columns j0..j0+bw-1 of tile X): rows j0..nb-1 at
-// Vbuf[(r - j0) + l*ldv]. Issued asynchronously; fix_v_geqrt (after the wait)
-// sets the unit diagonal, zeros above it and the k4 padding rows.
-__device__ __forceinline__ void issue_v_geqrt(double *V, int ldv, const double *X, int nb, int j0, int bw) {
-  async_block(V, ldv, X, nb, j0, nb, j0, bw);
+// ---- TMA: 3-D tensor copies in the row-tile layout ---------------------------
+// The host encodes A (and C) as a 3-D tensor (row within a tile of 8, global
+// column (k p + i) nb + c, row tile) with strides (8 B, nb * 8 B, 64 B); a box
+// of 8 x 32 x 4 lands in shared memory as 4 row tiles of 32 columns, i.e.
+// exactly the row-tile layout. Rows past nb (row tiles >= nb/8) are
+// out-of-bounds and filled with zeros by the copy engine.
+__device__ __forceinline__ void tma_box(double *dst, const CUtensorMap *map, int col, int tile, int b) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(0), "r"(col), "r"(tile), "r"(smem_u32(&s_mbar[b]))
+      : "memory");
 }
-// (bw <= 32: the column loops unroll into 4 predicated steps per warp)
-__device__ __forceinline__ void fix_v_geqrt(double *V, int ldv, int nb, int j0, int bw) {
-  const int nr = nb - j0, pad = ((nr + 15) & ~15) - nr;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int li = 0; li < 4; ++li) {
-    const int l = warp + li * kWarps;
-    if (l < bw) {
-      if (lane <= l && lane < nr) V[lane + l * ldv] = lane == l ? 1.0 : 0.0;
-      if (lane < pad) V[nr + lane + l * ldv] = 0.0;
-    }
-  }
+__device__ __forceinline__ void tma_bulk(double *dst, const double *src, unsigned bytes, int b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(&s_mbar[b]))
+               : "memory");
 }
-// V2 of a TTQRT (tri) / TSQRT block: rows 0..R2-1 of tile X, R2 = j0+bw (TT) or nb (TS);
-// in TT only the upper triangle (r <= j0+l) belongs to the reflectors.
-__device__ __forceinline__ void issue_v_tp(double *V, int ldv, const double *X, int nb, int j0, int bw, bool tri) {
-  async_block(V, ldv, X, nb, 0, tri ? j0 + bw : nb, j0, bw);
+__device__ __forceinline__ void mbar_expect_tx(int b, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_mbar[b])), "r"(bytes)
+               : "memory");
 }
-__device__ __forceinline__ void fix_v_tp(double *V, int ldv, int nb, int j0, int bw, bool tri) {
-  const int nr = tri ? j0 + bw : nb, pad = ((nr + 15) & ~15) - nr;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int li = 0; li < 4; ++li) {
-    const int l = warp + li * kWarps;
-    if (l < bw) {
-      if (tri && lane > l && lane < bw) V[j0 + lane + l * ldv] = 0.0;
-      if (lane < pad) V[nr + lane + l * ldv] = 0.0;
-    }
-  }
-}
-// zero V rows [nr, round_up(nr, 16)) of columns 0..bw-1 (K padding of the DMMA loops)
-__device__ __forceinline__ void zero_vpad(double *V, int ldv, int nr, int bw) {
-  const int pad = ((nr + 15) & ~15) - nr;
-  if (pad > 0) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int l = warp; l < bw; l += kWarps)
-      if (lane < pad) V[nr + lane + l * ldv] = 0.0;
-  }
-}
-// T block (bw x bw upper triangular) of columns j0.. of a T slot -> Ts (ld kTld);
-// the rest of the 32 x 32 block is zeroed (it feeds a padded DMMA)
-__device__ __forceinline__ void issue_t(double *Ts, const double *Tslot, int ib, int j0, int bw) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double *d0 = Ts + lane + warp * kTld;
-  const double *g0 = Tslot + lane + (size_t)(j0 + warp) * ib;
-#pragma unroll
-  for (int ci = 0; ci < 4; ++ci) {
-    const int c = warp + ci * kWarps;
-    if (lane <= c && c < bw) cp_async8(d0 + ci * kWarps * kTld, g0 + (size_t)ci * kWarps * ib);
-    else d0[ci * kWarps * kTld] = 0.0;
-  }
+// order this thread's earlier generic-proxy accesses (global data published by
+// other SMs and acquired by this CTA; shared-memory writes of this CTA) before
+// its next async-proxy (TMA) copies
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // ---- FP64 tensor-core MMA (DMMA): D(16x8) += A(16x4) B(4x8) ------------------
@@ -356,191 +258,6 @@ __device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, doubl
   asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
                : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
                : "d"(a0), "d"(a1), "d"(b0));
-}
-
-// ---- apply one compact-WY block to a strip held in shared memory ----------
-// W = [Ctop +] V^T Cv ; W2 = -op(T) W ; Cv += V W2 ; [Ctop += W2]
-// trans: op(T) = T^T (applies Q_b^T), else T (applies Q_b).
-// Ctop (bw rows, may be null) carries the implicit identity part of
-// V = [I; V2] (TT/TS kernels). All arrays in smem, column-major.
-// Requirements (kept by the loaders): V rows [nrows, round_up(nrows,4)) are
-// zero; everything the m16/n8 padding reads is finite; W/W2 have ldw = 36.
-// All three contractions run on the FP64 tensor pipe (mma.sync m16n8k4 f64).
-// DMMA latency (~150 cycles) is hidden with several independent accumulator
-// chains per warp: K is interleaved over 4 chains in phase 1 and 2 chains in
-// phase 2, and phase 3 deals the (m16, n8) fragments round-robin over warps
-// (warp w: n-tile w mod NT, m-tiles w / NT + i * 8 / NT).
-// Cv += V W2 for NF fragments (m-tiles mfirst, mfirst+MSTEP, ...) of n-tile n
-template <int NF, int MSTEP>
-__device__ __forceinline__ void phase3_frags(double *Cv, int ldc, int nrows, const double *V, int ldv,
-                                             const double *W2, int wsz, int n, int mfirst, int kpad3) {
-  constexpr int ldw = 36;
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int c0 = n * 8 + 2 * t;
-  double acc[NF][4];
-#pragma unroll
-  for (int i = 0; i < NF; ++i) {
-    const int m0 = (mfirst + i * MSTEP) * 16;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) acc[i][e] = Cv[(m0 + g + (e >> 1) * 8) + (c0 + (e & 1)) * ldc];
-  }
-  // K = 32 always (W2 rows >= bw are exact zeros); loads of step k+4 overlap the DMMAs of step k
-  const double *wb = W2 + t + (n * 8 + g) * ldw;
-  const double *vr = V + g + t * ldv + mfirst * 16;
-  double b = wb[0], a0[NF], a1[NF];
-#pragma unroll
-  for (int i = 0; i < NF; ++i) { a0[i] = vr[i * MSTEP * 16]; a1[i] = vr[i * MSTEP * 16 + 8]; }
-#pragma unroll
-  for (int k = 4; k < 32; k += 4) {
-    const double nbv = wb[k];
-    double n0[NF], n1[NF];
-#pragma unroll
-    for (int i = 0; i < NF; ++i) {
-      n0[i] = vr[i * MSTEP * 16 + k * ldv];
-      n1[i] = vr[i * MSTEP * 16 + 8 + k * ldv];
-    }
-#pragma unroll
-    for (int i = 0; i < NF; ++i) dmma(acc[i], a0[i], a1[i], b);
-    b = nbv;
-#pragma unroll
-    for (int i = 0; i < NF; ++i) { a0[i] = n0[i]; a1[i] = n1[i]; }
-  }
-#pragma unroll
-  for (int i = 0; i < NF; ++i) dmma(acc[i], a0[i], a1[i], b);
-  (void)kpad3;
-#pragma unroll
-  for (int i = 0; i < NF; ++i) {
-    const int m0 = (mfirst + i * MSTEP) * 16;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int r = m0 + g + (e >> 1) * 8, c = c0 + (e & 1);
-      if (r < nrows && c < wsz) Cv[r + c * ldc] = acc[i][e];
-    }
-  }
-}
-
-template <int NT>
-__device__ void apply_block_t(double *Ctop, double *Cv, int ldc, int nrows, const double *V, int ldv,
-                              const double *Ts, int bw, int wsz, bool trans, double *W, double *W2) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  constexpr int ldw = 36;
-  const int nt = (wsz + 7) >> 3;
-  // phase 1: W (bw x wsz) = V^T Cv, one 16x8 fragment per warp-iteration, full K in 4 chains
-  {
-    const int mt = (bw + 15) >> 4;
-    const int kpad = (nrows + 15) & ~15;        // V rows [nrows, kpad) are zero
-    for (int f = warp; f < mt * nt; f += kWarps) {
-      // bw <= 32, so mt is 1 or 2: no integer division
-      const int m0 = (mt == 2 ? (f & 1) : 0) * 16, n0 = (mt == 2 ? (f >> 1) : f) * 8;
-      double acc[4][4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[u][e] = 0.0;
-      const double *va = V + (m0 + g) * ldv + t;
-      const double *vb = va + 8 * ldv;
-      const double *cb = Cv + (n0 + g) * ldc + t;
-      // branch-free, software-pipelined: the fragments of step k+16 are loaded
-      // while the DMMAs of step k run (DMMAs under a branch do not overlap)
-      double fa[4], fb[4], fc[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) { fa[u] = va[4 * u]; fb[u] = vb[4 * u]; fc[u] = cb[4 * u]; }
-      for (int k = 16; k < kpad; k += 16) {
-        double na[4], nb2[4], nc[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) { na[u] = va[k + 4 * u]; nb2[u] = vb[k + 4 * u]; nc[u] = cb[k + 4 * u]; }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) dmma(acc[u], fa[u], fb[u], fc[u]);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) { fa[u] = na[u]; fb[u] = nb2[u]; fc[u] = nc[u]; }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) dmma(acc[u], fa[u], fb[u], fc[u]);
-      const int r0 = m0 + g, c0 = n0 + 2 * t;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int r = r0 + (e >> 1) * 8, c = c0 + (e & 1);
-        double v = (acc[0][e] + acc[1][e]) + (acc[2][e] + acc[3][e]);
-        if (Ctop && r < bw && c < wsz) v += Ctop[r + c * ldc];
-        W[r + c * ldw] = v;
-      }
-    }
-  }
-  __syncthreads();
-  prof_mark(PH_MMA1);
-  // phase 2: W2 = -op(T) W on the tensor pipe (T is a zero-padded 32 x 32
-  // upper triangle, so rows bw..31 of W2 come out exactly zero)
-  const int kpad3 = (bw + 3) & ~3;
-  for (int f = warp; f < 2 * nt; f += kWarps) {
-    const int m0 = (f & 1) * 16, n0 = (f >> 1) * 8;
-    double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
-    // K = 32 always: T is zero beyond bw, so the padding adds exact zeros
-#pragma unroll
-    for (int kk = 0; kk < 32; kk += 4) {
-      double a0, a1;
-      if (trans) {   // A[l][m] = T[m][l]
-        a0 = Ts[(kk + t) + (m0 + g) * kTld];
-        a1 = Ts[(kk + t) + (m0 + g + 8) * kTld];
-      } else {       // A[l][m] = T[l][m]
-        a0 = Ts[(m0 + g) + (kk + t) * kTld];
-        a1 = Ts[(m0 + g + 8) + (kk + t) * kTld];
-      }
-      dmma(acc[(kk >> 2) & 1], a0, a1, W[(kk + t) + (n0 + g) * ldw]);
-    }
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int r = m0 + g + (e >> 1) * 8, c = n0 + 2 * t + (e & 1);
-      W2[r + c * ldw] = -(acc[0][e] + acc[1][e]);
-    }
-  }
-  __syncthreads();
-  prof_mark(PH_TRI);
-  // phase 3: Cv (nrows x wsz) += V W2, fragments dealt round-robin; the
-  // per-warp fragment count selects a static-trip-count instance
-  {
-    constexpr int MSTEP = kWarps / NT;
-    const int mt = (nrows + 15) >> 4;
-    const int n = warp % NT, mfirst = warp / NT;
-    const int nf = mt > mfirst ? (mt - mfirst + MSTEP - 1) / MSTEP : 0;
-    if (n < nt && nf > 0) {
-      switch (nf) {
-        case 1: phase3_frags<1, MSTEP>(Cv, ldc, nrows, V, ldv, W2, wsz, n, mfirst, kpad3); break;
-        case 2: phase3_frags<2, MSTEP>(Cv, ldc, nrows, V, ldv, W2, wsz, n, mfirst, kpad3); break;
-        case 3: phase3_frags<3, MSTEP>(Cv, ldc, nrows, V, ldv, W2, wsz, n, mfirst, kpad3); break;
-        case 4: phase3_frags<4, MSTEP>(Cv, ldc, nrows, V, ldv, W2, wsz, n, mfirst, kpad3); break;
-        case 5: phase3_frags<5, MSTEP>(Cv, ldc, nrows, V, ldv, W2, wsz, n, mfirst, kpad3); break;
-        case 6: phase3_frags<6, MSTEP>(Cv, ldc, nrows, V, ldv, W2, wsz, n, mfirst, kpad3); break;
-        case 7: phase3_frags<7, MSTEP>(Cv, ldc, nrows, V, ldv, W2, wsz, n, mfirst, kpad3); break;
-        default: phase3_frags<8, MSTEP>(Cv, ldc, nrows, V, ldv, W2, wsz, n, mfirst, kpad3); break;
-      }
-    }
-  }
-  if (Ctop) {
-    for (int c = warp; c < wsz; c += kWarps)
-      if (lane < bw) Ctop[lane + c * ldc] += W2[lane + c * ldw];
-  }
-  __syncthreads();
-  prof_mark(PH_MMA3);
-}
-
-__device__ __forceinline__ void apply_block(double *Ctop, double *Cv, int ldc, int nrows, const double *V,
-                                            int ldv, const double *Ts, int bw, int wsz, bool trans, double *W,
-                                            double *W2) {
-  if (wsz <= 32) apply_block_t<4>(Ctop, Cv, ldc, nrows, V, ldv, Ts, bw, wsz, trans, W, W2);
-  else apply_block_t<8>(Ctop, Cv, ldc, nrows, V, ldv, Ts, bw, wsz, trans, W, W2);
-}
-
-// ---- warp reduce-scatter: lane l ends with sum over lanes of v[l] (v[0]) ----
-template <int OFF>
-__device__ __forceinline__ void rs_step(double (&v)[32], int lane) {
-  const bool hi = lane & OFF;
-#pragma unroll
-  for (int i = 0; i < OFF; ++i) {
-    double keep = hi ? v[i + OFF] : v[i];
-    double send = hi ? v[i] : v[i + OFF];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, OFF);
-  }
 }
 
 // ---- Householder scalars (xLARFG) from alpha and ||x||^2 ------------------
@@ -603,17 +320,21 @@ __device__ void t_doubling(double *Ts, const double *G, double *X) {
   }
 }
 
-// G (32 x 32, ld kTld) = V^T V for the 32 V columns in Vbuf (rows 0..nr4-1), DMMA
-__device__ void gram_v(double *G, const double *V, int ldv, int nr) {
+// G (32 x 32, ld kTld) = V^T V over row tiles [tlo, thi) of a row-tile-layout V
+// block (rows outside the reflectors are zero), on the tensor pipe: the two
+// k-steps of a tile take rows (2t) and (2t+1), one 16-byte load per operand.
+__device__ void gram_v8(double *G, const double *V, int tlo, int thi) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int m0 = (warp & 1) * 16, n0 = (warp >> 1) * 8;   // 8 warps = 2 x 4 fragments
-  const int kpad = (nr + 15) & ~15;          // rows [nr, kpad) of V are zero
   double acc0[4] = {0.0, 0.0, 0.0, 0.0}, acc1[4] = {0.0, 0.0, 0.0, 0.0};
-  const double *va = V + (m0 + g) * ldv + t, *vb = va + 8 * ldv, *vc = V + (n0 + g) * ldv + t;
-  for (int k = 0; k < kpad; k += 8) {
-    dmma(acc0, va[k], vb[k], vc[k]);
-    dmma(acc1, va[k + 4], vb[k + 4], vc[k + 4]);
+  for (int j = tlo; j < thi; ++j) {
+    const double *vt = V + j * 256 + 2 * t;
+    const double2 a = *reinterpret_cast<const double2 *>(vt + (m0 + g) * 8);
+    const double2 a8 = *reinterpret_cast<const double2 *>(vt + (m0 + g + 8) * 8);
+    const double2 b = *reinterpret_cast<const double2 *>(vt + (n0 + g) * 8);
+    dmma(acc0, a.x, a8.x, b.x);
+    dmma(acc1, a.y, a8.y, b.y);
   }
 #pragma unroll
   for (int e = 0; e < 4; ++e) G[(m0 + g + (e >> 1) * 8) + (n0 + 2 * t + (e & 1)) * kTld] = acc0[e] + acc1[e];
@@ -632,8 +353,9 @@ __device__ void gram_v(double *G, const double *V, int ldv, int nr) {
 // columns > c (warp-local dot products). The owner of column c+1 can start
 // as soon as its column is updated, so the per-column chain is short.
 // After the columns: G = V^T V on the tensor pipe and T by recursive
-// doubling. Writes R/V back (only the parts this kernel owns), fills Vbuf (for
-// a trailing update), Ts and the T slot.
+// doubling. Writes R/V back (only the parts this kernel owns), the T slot, and
+// leaves the block's V (row-tile layout, absolute rows, zero outside the
+// reflectors) in Vbuf and its T (ld ib) in Tb for a trailing update on this CTA.
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -642,10 +364,11 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 template <int MODE>
 __device__ void panel_block(double *X, double *A1, double *Tslot, int nb, int ib, int j0, int bw,
-                            double *Vbuf, int ldv, double *Ts, double *scratch) {
+                            double *Vbuf, double *Tb, double *scratch) {
   double *top = scratch;               // 32 x kTld scratch for t_doubling
   double *G = top + 32 * kTld;         // 32 x kTld: V^T V
-  double *vsh = G + 32 * kTld;         // 2 x 256: published reflector (double-buffered)
+  double *Ts = G + 32 * kTld;          // 32 x kTld: working T
+  double *vsh = Ts + 32 * kTld;        // 2 x 256: published reflector (double-buffered)
   double *scal = vsh + 2 * 256;        // 2 x 4: tau of the published reflector
   double *taus = scal + 8;             // 32
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -740,6 +463,10 @@ __device__ void panel_block(double *X, double *A1, double *Tslot, int nb, int ib
     }
   }
   // ---- write back the owned columns: X (R above / V below the pivot) and Vbuf ----
+  // Vbuf covers the whole row tiles [vlo, vhi) of the block's V rows, zero
+  // outside the reflectors (the gram product and the trailing update read
+  // whole tiles).
+  const int vlo = MODE == 0 ? (j0 & ~7) : 0, vhi = round_up(rbase + nr, 8);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int cl = warp + 8 * q;
@@ -752,14 +479,17 @@ __device__ void panel_block(double *X, double *A1, double *Tslot, int nb, int ib
           if (MODE == 0) {
             const double fin = rr == cl ? betas[q] : a[q][s2];
             X[row + (size_t)(j0 + cl) * nb] = fin;
-            Vbuf[rr + cl * ldv] = rr == cl ? 1.0 : (rr > cl ? a[q][s2] : 0.0);
+            Vbuf[vidx(row, cl)] = rr == cl ? 1.0 : (rr > cl ? a[q][s2] : 0.0);
           } else {
             const bool part = MODE == 2 || row <= j0 + cl;
             if (part) X[row + (size_t)(j0 + cl) * nb] = a[q][s2];
-            Vbuf[rr + cl * ldv] = part ? a[q][s2] : 0.0;
+            Vbuf[vidx(row, cl)] = part ? a[q][s2] : 0.0;
           }
+        } else if (row < vhi) {
+          Vbuf[vidx(row, cl)] = 0.0;
         }
       }
+      if (MODE == 0 && lane < j0 - vlo) Vbuf[vidx(vlo + lane, cl)] = 0.0;
     }
   }
   if (MODE != 0) {     // final pivot rows (R) back to A1, upper triangle of the block
@@ -769,179 +499,410 @@ __device__ void panel_block(double *X, double *A1, double *Tslot, int nb, int ib
       if (cl < bw && lane <= cl) A1[(j0 + lane) + (size_t)(j0 + cl) * nb] = pt[q];
     }
   }
-  __syncthreads();
-  zero_vpad(Vbuf, ldv, nr, bw);
   for (int idx = tid; idx < 32 * 32; idx += kThreads) {     // Ts = diag(tau) (zero-padded)
     const int l = idx & 31, c = idx >> 5;
     Ts[l + c * kTld] = (l == c && c < bw) ? taus[c] : 0.0;
   }
   __syncthreads();
   prof_mark(PH_PANEL);
-  gram_v(G, Vbuf, ldv, nr);
+  gram_v8(G, Vbuf, vlo >> 3, vhi >> 3);
   __syncthreads();
   t_doubling(Ts, G, top);
   prof_mark(PH_TREC);
   for (int c = warp; c < bw; c += kWarps)
-    if (lane < ib) Tslot[lane + (size_t)(j0 + c) * ib] = (lane < bw && lane <= c) ? Ts[lane + c * kTld] : 0.0;
+    if (lane < ib) {
+      const double v = (lane < bw && lane <= c) ? Ts[lane + c * kTld] : 0.0;
+      Tslot[lane + (size_t)(j0 + c) * ib] = v;
+      Tb[lane + c * ib] = v;
+    }
 }
 
-// ---- panel kernels: GEQRT / TTQRT / TSQRT on whole tiles ------------------
-template <int MODE>
-__device__ void panel_task(double *X, double *A1, double *Tslot, int nb, int ib, int ws, double *smem,
-                           const SmemLayout &L) {
-  double *Cb = smem + L.offC, *Vb = smem + L.offV[0], *Wb = smem + L.offW, *Ts = smem + L.offT[0];
-  for (int j0 = 0; j0 < nb; j0 += ib) {
-    const int bw = min(ib, nb - j0);
-    panel_block<MODE>(X, A1, Tslot, nb, ib, j0, bw, Vb, L.ldv, Ts, Wb);
-    // trailing update of columns j0+bw..nb-1 with Q_b^T
-    for (int cs = j0 + bw; cs < nb; cs += ws) {
-      const int wsz = min(ws, nb - cs);
-      __syncthreads();
-      if (MODE == 0) {
-        load_rows(Cb, L.ldc, 0, X, nb, j0, nb, cs, wsz);
-        cp_async_wait_all();
-        __syncthreads();
-        prof_mark(PH_LOAD);
-        apply_block(nullptr, Cb + j0, L.ldc, nb - j0, Vb, L.ldv, Ts, bw, wsz, true, Wb, Wb + L.ldw * L.wcols);
-        store_rows(Cb, L.ldc, 0, X, nb, j0, nb, cs, wsz);
-      } else {
-        const int r2 = MODE == 1 ? j0 + bw : nb;
-        async_block(Cb, L.ldc, A1, nb, j0, j0 + bw, cs, wsz);         // C1 rows of the block -> window 0
-        load_rows(Cb, L.ldc, kWinRows, X, nb, 0, r2, cs, wsz);
-        cp_async_wait_all();
-        __syncthreads();
-        prof_mark(PH_LOAD);
-        apply_block(Cb, Cb + kWinRows, L.ldc, r2, Vb, L.ldv, Ts, bw, wsz, true, Wb, Wb + L.ldw * L.wcols);
-        store_rows(Cb - j0, L.ldc, 0, A1, nb, j0, j0 + bw, cs, wsz);
-        store_rows(Cb, L.ldc, kWinRows, X, nb, 0, r2, cs, wsz);
+// ---- trailing updates on one column strip (UNMQR / TTMQR / TSMQR) -----------
+// C <- Q_b^T C (or Q_b C) for the inner blocks b of a panel kernel's
+// reflectors, in compact-WY form (lines 62-66): W = V^T C, W2 = -op(T) W,
+// C += V W2; for TT/TS (V = [I; V2], Table 1) W = C1_b + V2^T C2,
+// C1_b += W2, C2 += V2 W2.
+//
+// Register-resident design: the strip's C (C2 for TT/TS) lives in registers
+// as fragments of C^T for the whole task; only V, T and the 32-row C1 window
+// of each inner block move through shared memory (double-buffered, the next
+// block's copies in flight during this block's math). Warp w = (row group
+// rg = w/2, column half mh = w%2) owns columns 16 mh .. 16 mh + 15 of the row
+// tiles j = rg + 4 s (s < kSlots). Per block:
+//   phase 1  partial W^T over the warp's row tiles: the C^T accumulators ARE
+//            the A fragments (k-steps = rows 2t and 2t+1 of a tile), V the B
+//            fragments (one 16-byte load per 2 DMMAs); 4 partials -> smem
+//   reduce   W^T = sum of the partials (+ C1 window for TT/TS)
+//   phase 2  W2^T = -W^T op(T)^T, one 16x8 fragment per warp, + C1_b update
+//   phase 3  C^T += W2^T V^T (V^T from smem, W2^T fragments held in registers)
+// All contractions run on the FP64 tensor pipe (mma.sync m16n8k4 f64 = DMMA).
+// The reflectors' structure (unit diagonal / zeros above it for GEQRT, the
+// upper trapezoid of TTQRT) is applied as a mask on the loaded fragments of
+// the <= 5 row tiles that cross the block's diagonal, so V is copied raw.
+enum { SU_UN = 0, SU_TT = 1, SU_TS = 2 };
+
+struct StripJob {
+  const double *Vt;     // tile holding the reflectors (GEQRT: V below the diagonal; TT/TS: V2)
+  const double *Tslot;  // its T slot (ib x nb, ld ib)
+  double *C1;           // TT/TS: the pivot-row tile (rows b*ib .. b*ib + bw - 1 per block)
+  double *C2;           // the updated tile
+  int nb, ib, cs, wsz;  // strip = columns [cs, cs + wsz) of C1 / C2
+  int b_lo, b_hi;       // inner blocks applied (ascending for Q^T, descending for Q)
+  bool trans, resident; // resident: block b_lo's V and T are already in buffer 0 (panel chain)
+  const CUtensorMap *mV, *mC;   // TMA path: tensor maps of the V tile's and the C tiles' matrix (null: cp.async)
+  int vcol, c1col;              // global column of the V tile's and the C1 tile's first column
+};
+
+// row tiles a block touches: UN rows j0..nb-1, TT rows 0..j0+bw-1, TS rows 0..nb-1
+template <int KIND>
+__device__ __forceinline__ void su_range(int j0, int bw, int ntile, int &lo, int &hi) {
+  lo = KIND == SU_UN ? (j0 >> 3) : 0;
+  hi = KIND == SU_TT ? ((j0 + bw + 7) >> 3) : ntile;
+}
+// V element (row r, reflector l) of block j0 from its raw tile value
+template <int KIND>
+__device__ __forceinline__ double vmask(double v, int r, int l, int j0) {
+  if (KIND == SU_UN) {
+    const int rr = r - j0;
+    return rr > l ? v : (rr == l ? 1.0 : 0.0);
+  }
+  return r <= j0 + l ? v : 0.0;
+}
+
+// copies of block b into buffer `buf` (all threads; one mbarrier arrival each);
+// vt = false: V and T are already there (panel chain), only the C1 window moves
+template <int KIND>
+__device__ __forceinline__ void su_issue(const StripJob &J, const SmemLayout &L, double *smem, int buf, int b,
+                                         bool vt = true) {
+  const int j0 = b * J.ib, bw = min(J.ib, J.nb - j0);
+  int lo, hi;
+  su_range<KIND>(j0, bw, L.ntile, lo, hi);
+  if (J.mV) {
+    // one thread issues: V as 4-tile boxes ending at row tile hi (a box never
+    // leaves [0, ntile): ntile >= 4 on this path), T as one bulk copy, the C1
+    // window as one 4-tile box at row tile j0/8 (j0 % 8 == 0 on this path)
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      const int nv = vt ? (hi - lo + 3) >> 2 : 0;
+      const unsigned tbytes = vt ? (unsigned)(bw * J.ib) * 8u : 0u;
+      mbar_expect_tx(buf, (unsigned)nv * 8192u + tbytes + (KIND != SU_UN ? 8192u : 0u));
+      double *V = smem + L.offV[buf];
+      for (int e = hi, x = 0; x < nv; ++x, e -= 4) {
+        const int st = e - 4 > 0 ? e - 4 : 0;
+        tma_box(V + st * 256, J.mV, J.vcol + j0, st, buf);
+      }
+      if (vt) tma_bulk(smem + L.offT[buf], J.Tslot + (size_t)j0 * J.ib, tbytes, buf);
+      if (KIND != SU_UN) tma_box(smem + L.offC1[buf], J.mC, J.c1col + J.cs, j0 >> 3, buf);
+    }
+  } else {
+    if (vt) {
+      load_tiles8(smem + L.offV[buf] + lo * 256, J.Vt, J.nb, 8 * lo, hi - lo, j0, bw);
+      load_tblock(smem + L.offT[buf], J.Tslot, J.ib, j0, bw);
+    }
+    if (KIND != SU_UN) load_tiles8(smem + L.offC1[buf], J.C1, J.nb, j0, (bw + 7) >> 3, J.cs, J.wsz);
+  }
+  mbar_arrive_cp(buf);
+}
+
+// Row tile of slot s of row group rg. Slots are dealt so that the tiles a
+// block touches are always a PREFIX of every warp's slots (UN: bottom-up, since
+// block b touches rows j0..nb-1; TT/TS: top-down, rows 0..): the math then runs
+// as fully unrolled instances for n = 0..kSlots active slots without a
+// per-slot guard around the DMMAs (a DMMA under a runtime branch serialises).
+template <int KIND>
+__device__ __forceinline__ int su_tile(int rg, int s, int ntile) {
+  return KIND == SU_UN ? ntile - 1 - rg - 4 * s : rg + 4 * s;
+}
+// active slots of row group rg when the touched row tiles are [lo, hi)
+template <int KIND>
+__device__ __forceinline__ int su_nact(int rg, int lo, int hi, int ntile) {
+  const int R = KIND == SU_UN ? ntile - lo : hi;
+  return R > rg ? (R - rg + 3) >> 2 : 0;
+}
+
+// phase 1 on N slots: partial W^T (16 columns x 32 reflectors) += C^T V
+template <int KIND, int N>
+__device__ __forceinline__ void su_p1(const double (&acc)[kSlots][4], double (&w)[4][4], double *Vb, int rg,
+                                      int ntile, int j0, int band_lo, int band_hi, bool wb) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int s = 0; s < N; ++s) {
+    const int j = su_tile<KIND>(rg, s, ntile);
+    double *vt = Vb + j * 256 + g * 8 + 2 * t;
+    double2 bv[4];
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn) bv[nn] = *reinterpret_cast<const double2 *>(vt + 64 * nn);
+    // the band tiles (<= 5, crossing the block's diagonal) are always among
+    // the last two active slots: mask them here and store the masked tile back
+    // (column half 0's warp) so phase 3 reads a clean V
+    if (KIND != SU_TS && s + 2 >= N && j < band_hi && j >= band_lo) {
+      const int r = 8 * j + 2 * t;
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn) {
+        bv[nn].x = vmask<KIND>(bv[nn].x, r, 8 * nn + g, j0);
+        bv[nn].y = vmask<KIND>(bv[nn].y, r + 1, 8 * nn + g, j0);
+      }
+      if (wb) {
+#pragma unroll
+        for (int nn = 0; nn < 4; ++nn) *reinterpret_cast<double2 *>(vt + 64 * nn) = bv[nn];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // before a later TMA refill of this buffer
+      }
+    }
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn) dmma(w[nn], acc[s][0], acc[s][2], bv[nn].x);
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn) dmma(w[nn], acc[s][1], acc[s][3], bv[nn].y);
+  }
+}
+// phase 3 on N slots: C^T += W2^T V^T (W2^T fragments wa0/wa1 per k-step; V already masked)
+template <int KIND, int N>
+__device__ __forceinline__ void su_p3(double (&acc)[kSlots][4], const double (&wa0)[8], const double (&wa1)[8],
+                                      const double *Vb, int rg, int ntile) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    double bb[N > 0 ? N : 1];
+#pragma unroll
+    for (int s = 0; s < N; ++s) {
+      const int j = su_tile<KIND>(rg, s, ntile);
+      bb[s] = Vb[j * 256 + (4 * kk + t) * 8 + g];
+    }
+#pragma unroll
+    for (int s = 0; s < N; ++s) dmma(acc[s], wa0[kk], wa1[kk], bb[s]);
+  }
+}
+
+#define TQR_SLOT_SWITCH(n, CALL)                                                            \
+  switch (n) {                                                                              \
+    case 1: CALL(1); break; case 2: CALL(2); break; case 3: CALL(3); break;                 \
+    case 4: CALL(4); break; case 5: CALL(5); break; case 6: CALL(6); break;                 \
+    case 7: CALL(7); break; case 8: CALL(8); break; default: break;                         \
+  }
+
+template <int KIND>
+__device__ void strip_update(const StripJob &J, double *smem, const SmemLayout &L, unsigned &ph) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int rg = warp >> 1, mh = warp & 1, cg = 16 * mh + g;
+  const int mt = warp & 1, nt = warp >> 1;            // phase-2 fragment of this warp
+  const int nb = J.nb, ib = J.ib, ntile = L.ntile, wsz = J.wsz;
+  const int nblk = J.b_hi - J.b_lo;
+  const bool even = (nb & 1) == 0;
+  int ct_lo = 0, ct_hi = ntile;                       // row tiles of C this task touches
+  if (KIND == SU_UN) ct_lo = (J.b_lo * ib) >> 3;
+  if (KIND == SU_TT) ct_hi = (min(J.b_hi * ib, nb) + 7) >> 3;
+  const int ntask = su_nact<KIND>(rg, ct_lo, ct_hi, ntile);   // slots holding C rows of this task
+  const bool wait0 = !J.resident || KIND != SU_UN;     // resident TT/TS blocks still load their C1 window
+  if (wait0) su_issue<KIND>(J, L, smem, 0, J.trans ? J.b_lo : J.b_hi - 1, !J.resident);
+
+  // C strip -> registers: acc[s] = C^T fragment (columns cg, cg+8; rows 8j+2t, 8j+2t+1)
+  double acc[kSlots][4];
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) {
+    const int j = su_tile<KIND>(rg, s, ntile), r = 8 * j + 2 * t;
+    const bool act = s < ntask && r < nb;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int col = cg + 8 * h;
+      double x0 = 0.0, x1 = 0.0;
+      if (act && col < wsz) {
+        const double *src = J.C2 + r + (size_t)(J.cs + col) * nb;
+        if (even) {
+          const double2 v = __ldcg(reinterpret_cast<const double2 *>(src));
+          x0 = v.x; x1 = v.y;
+        } else {
+          x0 = __ldcg(src);
+          if (r + 1 < nb) x1 = __ldcg(src + 1);
+        }
+      }
+      acc[s][2 * h] = x0;
+      acc[s][2 * h + 1] = x1;
+    }
+  }
+
+  for (int idx = 0; idx < nblk; ++idx) {
+    const int cur = idx & 1;
+    const int b = J.trans ? J.b_lo + idx : J.b_hi - 1 - idx;
+    const int j0 = b * ib, bw = min(ib, nb - j0);
+    int blo, bhi;
+    su_range<KIND>(j0, bw, ntile, blo, bhi);
+    const int nact = 16 * mh < wsz ? su_nact<KIND>(rg, blo, bhi, ntile) : 0;   // (a column half beyond a narrow strip idles)
+    const int band_lo = j0 >> 3, band_hi = (j0 + bw + 7) >> 3;   // tiles crossing the block's diagonal
+    if (idx > 0 || wait0) mbar_wait(cur, ph);
+    prof_mark(PH_LOAD);
+    double *Vb = smem + L.offV[cur];
+    const double *Tb = smem + L.offT[cur], *C1w = smem + L.offC1[cur];
+    // phase-2 B operand: op(T)^T fragments of this warp's n-tile (T upper triangular, zero-padded)
+    double tb[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int r = J.trans ? 4 * kk + t : 8 * nt + g, c = J.trans ? 8 * nt + g : 4 * kk + t;
+      tb[kk] = (r <= c && c < bw) ? Tb[r + c * ib] : 0.0;
+    }
+
+    // ---- phase 1: partial W^T (16 columns x 32 reflectors) over this warp's row tiles
+    double wacc[4][4];
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) wacc[nn][e] = 0.0;
+#define TQR_P1(N) su_p1<KIND, N>(acc, wacc, Vb, rg, ntile, j0, band_lo, band_hi, mh == 0)
+    TQR_SLOT_SWITCH(nact, TQR_P1)
+#undef TQR_P1
+    {
+      double *Wp = smem + L.offWp + rg * 32 * kLdw;
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn) {
+        const int rf = 8 * nn + 2 * t;
+        Wp[cg + rf * kLdw] = wacc[nn][0];
+        Wp[cg + (rf + 1) * kLdw] = wacc[nn][1];
+        Wp[cg + 8 + rf * kLdw] = wacc[nn][2];
+        Wp[cg + 8 + (rf + 1) * kLdw] = wacc[nn][3];
       }
     }
     __syncthreads();
+    prof_mark(PH_MMA1);
+    // the other buffer is free now (its last reader was the previous block's phase 3)
+    if (idx + 1 < nblk) su_issue<KIND>(J, L, smem, cur ^ 1, J.trans ? b + 1 : b - 1);
+
+    // ---- reduce the 4 partials (+ the C1 window: identity part of V)
+    {
+      double *W = smem + L.offW;
+      const double *Wp0 = smem + L.offWp;
+      const int r8 = lane & 7, c4 = lane >> 3;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int x = warp * 4 + i, rt = x >> 3, cb = x & 7;
+        const int refl = 8 * rt + r8, col = 4 * cb + c4, o = col + refl * kLdw;
+        double v = (Wp0[o] + Wp0[o + 32 * kLdw]) + (Wp0[o + 64 * kLdw] + Wp0[o + 96 * kLdw]);
+        if (KIND != SU_UN) v += C1w[rt * 256 + col * 8 + r8];
+        W[o] = v;
+      }
+    }
+    __syncthreads();
+    prof_mark(PH_FIX);
+
+    // ---- phase 2: W2^T fragment (columns 16 mt.., reflectors 8 nt..) = -W^T op(T)^T
+    {
+      const double *W = smem + L.offW;
+      double *W2 = smem + L.offW2;
+      double a2[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const double a0 = W[(16 * mt + g) + (4 * kk + t) * kLdw];
+        const double a1 = W[(16 * mt + g + 8) + (4 * kk + t) * kLdw];
+        dmma(a2[kk & 1], a0, a1, tb[kk]);
+      }
+      double w2[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) w2[e] = -(a2[0][e] + a2[1][e]);
+      const int rf = 8 * nt + 2 * t;
+      W2[(16 * mt + g) + rf * kLdw] = w2[0];
+      W2[(16 * mt + g) + (rf + 1) * kLdw] = w2[1];
+      W2[(16 * mt + g + 8) + rf * kLdw] = w2[2];
+      W2[(16 * mt + g + 8) + (rf + 1) * kLdw] = w2[3];
+      if (KIND != SU_UN) {   // C1_b rows j0 + rf, rf + 1 += W2 (straight to global)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = 16 * mt + g + 8 * h;
+          if (col < wsz && rf < bw) {
+            const double2 c1 = *reinterpret_cast<const double2 *>(C1w + nt * 256 + col * 8 + 2 * t);
+            double *dst = J.C1 + (j0 + rf) + (size_t)(J.cs + col) * nb;
+            const double v0 = c1.x + w2[2 * h], v1 = c1.y + w2[2 * h + 1];
+            if (rf + 1 < bw && ((nb | j0) & 1) == 0) {
+              *reinterpret_cast<double2 *>(dst) = make_double2(v0, v1);
+            } else {
+              dst[0] = v0;
+              if (rf + 1 < bw) dst[1] = v1;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    prof_mark(PH_TRI);
+
+    // ---- phase 3: C^T += W2^T V^T on this warp's row tiles
+    {
+      const double *W2 = smem + L.offW2;
+      double wa0[8], wa1[8];
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        wa0[kk] = W2[cg + (4 * kk + t) * kLdw];
+        wa1[kk] = W2[cg + 8 + (4 * kk + t) * kLdw];
+      }
+#define TQR_P3(N) su_p3<KIND, N>(acc, wa0, wa1, Vb, rg, ntile)
+      TQR_SLOT_SWITCH(nact, TQR_P3)
+#undef TQR_P3
+    }
+    prof_mark(PH_MMA3);
+  }
+
+  // ---- C strip back to global (only the rows and columns this task owns)
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) {
+    const int j = su_tile<KIND>(rg, s, ntile), r = 8 * j + 2 * t;
+    const bool act = s < ntask && r < nb;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int col = cg + 8 * h;
+      if (act && col < wsz) {
+        double *dst = J.C2 + r + (size_t)(J.cs + col) * nb;
+        if (even) {
+          *reinterpret_cast<double2 *>(dst) = make_double2(acc[s][2 * h], acc[s][2 * h + 1]);
+        } else {
+          dst[0] = acc[s][2 * h];
+          if (r + 1 < nb) dst[1] = acc[s][2 * h + 1];
+        }
+      }
+    }
   }
 }
 
-// ---- update kernels on one column strip -----------------------------------
-// Inner blocks are pipelined: while block b is applied, the V / T (and C1
-// rows) of the next block stream into the other buffer (when smem allows).
-
-// UNMQR: C (tile strip) <- Q^T C (or Q C) with inner blocks [b_lo, b_hi) of the
-// GEQRT reflectors of tile Vt; only rows >= b_lo*ib are touched.
-__device__ void unmqr_strip(const double *Vt, const double *Tslot, double *Ct, int nb, int ib, int cs,
-                            int wsz, bool trans, int b_lo, int b_hi, double *smem, const SmemLayout &L,
-                            unsigned &mbph, bool tma, bool resident = false) {
-  double *Cb = smem + L.offC, *Wb = smem + L.offW;
-  const int r0 = b_lo * ib;
-  const int nblk = b_hi - b_lo;
-  auto blk = [&](int idx) { return trans ? b_lo + idx : b_hi - 1 - idx; };
-  tma_block(Cb + r0, L.ldc, Ct, nb, r0, nb, cs, wsz, tma);
-  if (!resident) {     // resident: the panel task just left V (unit diagonal, padded) and T in buffer 0
-    const int j0 = blk(0) * ib, bw = min(ib, nb - j0);
-    tma_block(smem + L.offV[0], L.ldv, Vt, nb, j0, nb, j0, bw, tma);
-    issue_t(smem + L.offT[0], Tslot, ib, j0, bw);
-  }
-  for (int idx = 0; idx < nblk; ++idx) {
-    const int cur = idx & (L.nvb - 1);
-    double *Vb = smem + (cur ? L.offV[1] : L.offV[0]), *Ts = smem + (cur ? L.offT[1] : L.offT[0]);
-    const int j0 = blk(idx) * ib, bw = min(ib, nb - j0);
-    async_wait(mbph);
+// ---- panel kernels: GEQRT / TTQRT / TSQRT on whole tiles ------------------
+// (monolithic form, TQR_SPLIT=0: every block's trailing update runs here)
+template <int MODE>
+__device__ void panel_task(double *X, double *A1, double *Tslot, int nb, int ib, int ws, double *smem,
+                           const SmemLayout &L, unsigned &ph, const CUtensorMap *mA, int a1col) {
+  for (int j0 = 0; j0 < nb; j0 += ib) {
+    const int bw = min(ib, nb - j0);
+    panel_block<MODE>(X, A1, Tslot, nb, ib, j0, bw, smem + L.offV[0], smem + L.offT[0], smem + L.offWp);
     __syncthreads();
-    prof_mark(PH_LOAD);
-    if (!(resident && idx == 0)) {
-      fix_v_geqrt(Vb, L.ldv, nb, j0, bw);
+    for (int cs = j0 + bw; cs < nb; cs += ws) {
+      const StripJob J{X, Tslot, A1, X, nb, ib, cs, min(ws, nb - cs), j0 / ib, j0 / ib + 1, true, true, mA, mA, 0,
+                       a1col};
+      if (MODE == 0) strip_update<SU_UN>(J, smem, L, ph);
+      else if (MODE == 1) strip_update<SU_TT>(J, smem, L, ph);
+      else strip_update<SU_TS>(J, smem, L, ph);
       __syncthreads();
     }
-    prof_mark(PH_FIX);
-    if (L.nvb == 2 && idx + 1 < nblk) {
-      const int j1 = blk(idx + 1) * ib, bw1 = min(ib, nb - j1);
-      tma_block(smem + (cur ? L.offV[0] : L.offV[1]), L.ldv, Vt, nb, j1, nb, j1, bw1, tma);
-      issue_t(smem + (cur ? L.offT[0] : L.offT[1]), Tslot, ib, j1, bw1);
-    }
-    apply_block(nullptr, Cb + j0, L.ldc, nb - j0, Vb, L.ldv, Ts, bw, wsz, trans, Wb, Wb + L.ldw * L.wcols);
-    if (L.nvb == 1 && idx + 1 < nblk) {
-      const int j1 = blk(idx + 1) * ib, bw1 = min(ib, nb - j1);
-      tma_block(Vb, L.ldv, Vt, nb, j1, nb, j1, bw1, tma);
-      issue_t(Ts, Tslot, ib, j1, bw1);
-    }
   }
-  store_rows(Cb, L.ldc, 0, Ct, nb, r0, nb, cs, wsz);
-}
-
-// TTMQR / TSMQR: [C1; C2] <- Q^T [C1; C2] (or Q) with inner blocks [b_lo, b_hi)
-// of the TTQRT/TSQRT reflectors V2 of tile Vt. Block b touches C1 rows
-// b*ib .. b*ib+bw-1 (streamed through a 32-row window) and C2 rows
-// 0 .. (tri ? b*ib+bw : nb)-1 (resident).
-__device__ void tpmqr_strip(const double *Vt, const double *Tslot, double *C1, double *C2, int nb, int ib,
-                            int cs, int wsz, bool tri, bool trans, int b_lo, int b_hi, double *smem,
-                            const SmemLayout &L, unsigned &mbph, bool tma, bool resident = false) {
-  double *Cb = smem + L.offC, *Wb = smem + L.offW;
-  const int r2hi = tri ? min(b_hi * ib, nb) : nb;
-  const int nblk = b_hi - b_lo;
-  auto blk = [&](int idx) { return trans ? b_lo + idx : b_hi - 1 - idx; };
-  tma_block(Cb + kWinRows, L.ldc, C2, nb, 0, r2hi, cs, wsz, tma);
-  {
-    const int j0 = blk(0) * ib, bw = min(ib, nb - j0);
-    if (!resident) {
-      tma_block(smem + L.offV[0], L.ldv, Vt, nb, 0, tri ? j0 + bw : nb, j0, bw, tma);
-      issue_t(smem + L.offT[0], Tslot, ib, j0, bw);
-    }
-    tma_block(Cb, L.ldc, C1, nb, j0, j0 + bw, cs, wsz, tma);
-  }
-  for (int idx = 0; idx < nblk; ++idx) {
-    const int cur = idx & (L.nvb - 1);
-    double *Vb = smem + (cur ? L.offV[1] : L.offV[0]), *Ts = smem + (cur ? L.offT[1] : L.offT[0]), *win = Cb + 32 * (idx & 1);
-    const int j0 = blk(idx) * ib, bw = min(ib, nb - j0);
-    async_wait(mbph);
-    __syncthreads();
-    prof_mark(PH_LOAD);
-    if (!(resident && idx == 0)) {
-      fix_v_tp(Vb, L.ldv, nb, j0, bw, tri);
-      __syncthreads();
-    }
-    prof_mark(PH_FIX);
-    if (L.nvb == 2 && idx + 1 < nblk) {
-      const int j1 = blk(idx + 1) * ib, bw1 = min(ib, nb - j1);
-      tma_block(smem + (cur ? L.offV[0] : L.offV[1]), L.ldv, Vt, nb, 0, tri ? j1 + bw1 : nb, j1, bw1, tma);
-      issue_t(smem + (cur ? L.offT[0] : L.offT[1]), Tslot, ib, j1, bw1);
-      tma_block(Cb + 32 * ((idx + 1) & 1), L.ldc, C1, nb, j1, j1 + bw1, cs, wsz, tma);
-    }
-    apply_block(win, Cb + kWinRows, L.ldc, tri ? j0 + bw : nb, Vb, L.ldv, Ts, bw, wsz, trans, Wb,
-                Wb + L.ldw * L.wcols);
-    store_rows(win - j0, L.ldc, 0, C1, nb, j0, j0 + bw, cs, wsz);
-    if (L.nvb == 1 && idx + 1 < nblk) {
-      __syncthreads();
-      const int j1 = blk(idx + 1) * ib, bw1 = min(ib, nb - j1);
-      tma_block(Vb, L.ldv, Vt, nb, 0, tri ? j1 + bw1 : nb, j1, bw1, tma);
-      issue_t(Ts, Tslot, ib, j1, bw1);
-      tma_block(Cb + 32 * ((idx + 1) & 1), L.ldc, C1, nb, j1, j1 + bw1, cs, wsz, tma);
-    }
-  }
-  store_rows(Cb, L.ldc, kWinRows, C2, nb, 0, r2hi, cs, wsz);
 }
 
 __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const SmemLayout &L, bool resident,
-                         unsigned &mbph) {
-  const bool tma = a.tma != 0;
+                         unsigned &ph) {
   const int p = a.p, nb = a.nb, ib = a.ib, ws = a.ws;
   const int nblk = (nb + ib - 1) / ib;
-  double *Vb = smem + L.offV[0], *Wb = smem + L.offW, *Ts = smem + L.offT[0];
+  double *Vb = smem + L.offV[0], *Tb = smem + L.offT[0], *scr = smem + L.offWp;
+  const CUtensorMap *mA = a.tma ? &a.mapA : nullptr, *mC = a.tma ? &a.mapC : nullptr;
+  auto col = [&](int i, int k) { return (k * p + i) * nb; };   // global column of tile (i, k)
   switch (t.kind) {
     case K_GEQRT:
       panel_task<0>(tile_ptr(a.A, p, nb, t.i, t.k), nullptr, tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0), nb, ib, ws,
-                    smem, L);
+                    smem, L, ph, mA, 0);
       break;
     case K_TTQRT:
       panel_task<1>(tile_ptr(a.A, p, nb, t.i, t.k), tile_ptr(a.A, p, nb, t.piv, t.k),
-                    tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1), nb, ib, ws, smem, L);
+                    tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1), nb, ib, ws, smem, L, ph, mA, col(t.piv, t.k));
       break;
     case K_TSQRT:
       panel_task<2>(tile_ptr(a.A, p, nb, t.i, t.k), tile_ptr(a.A, p, nb, t.piv, t.k),
-                    tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1), nb, ib, ws, smem, L);
+                    tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1), nb, ib, ws, smem, L, ph, mA, col(t.piv, t.k));
       break;
     // ---- split panels: inner block s of the panel, or update of strip s by block j
     case K_GEQRT_B: {
       const int j0 = t.s * ib;
       panel_block<0>(tile_ptr(a.A, p, nb, t.i, t.k), nullptr, tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0), nb, ib, j0,
-                     min(ib, nb - j0), Vb, L.ldv, Ts, Wb);
+                     min(ib, nb - j0), Vb, Tb, scr);
       break;
     }
     case K_TTQRT_B:
@@ -949,32 +910,37 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
       const int j0 = t.s * ib;
       double *X = tile_ptr(a.A, p, nb, t.i, t.k), *A1 = tile_ptr(a.A, p, nb, t.piv, t.k);
       double *Tsl = tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1);
-      if (t.kind == K_TTQRT_B) panel_block<1>(X, A1, Tsl, nb, ib, j0, min(ib, nb - j0), Vb, L.ldv, Ts, Wb);
-      else panel_block<2>(X, A1, Tsl, nb, ib, j0, min(ib, nb - j0), Vb, L.ldv, Ts, Wb);
+      if (t.kind == K_TTQRT_B) panel_block<1>(X, A1, Tsl, nb, ib, j0, min(ib, nb - j0), Vb, Tb, scr);
+      else panel_block<2>(X, A1, Tsl, nb, ib, j0, min(ib, nb - j0), Vb, Tb, scr);
       break;
     }
     case K_GEQRT_U: {
-      const int cs = t.s * ws, wsz = min(ws, nb - cs);
+      const int cs = t.s * ws;
       double *X = tile_ptr(a.A, p, nb, t.i, t.k);
-      unmqr_strip(X, tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0), X, nb, ib, cs, wsz, true, t.j, t.j + 1, smem, L,
-                  mbph, tma, resident);
+      const StripJob J{X, tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0), nullptr, X, nb, ib, cs, min(ws, nb - cs),
+                       t.j, t.j + 1, true, resident, mA, mA, col(t.i, t.k), 0};
+      strip_update<SU_UN>(J, smem, L, ph);
       break;
     }
     case K_TTQRT_U:
     case K_TSQRT_U: {
-      const int cs = t.s * ws, wsz = min(ws, nb - cs);
+      const int cs = t.s * ws;
       double *X = tile_ptr(a.A, p, nb, t.i, t.k);
-      tpmqr_strip(X, tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1), tile_ptr(a.A, p, nb, t.piv, t.k), X, nb, ib, cs, wsz,
-                  t.kind == K_TTQRT_U, true, t.j, t.j + 1, smem, L, mbph, tma, resident);
+      const StripJob J{X, tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1), tile_ptr(a.A, p, nb, t.piv, t.k), X, nb, ib, cs,
+                       min(ws, nb - cs), t.j, t.j + 1, true, resident, mA, mA, col(t.i, t.k), col(t.piv, t.k)};
+      if (t.kind == K_TTQRT_U) strip_update<SU_TT>(J, smem, L, ph);
+      else strip_update<SU_TS>(J, smem, L, ph);
       break;
     }
     // ---- updates of other tiles (factorization) and of C (apply)
     case K_UNMQR:
     case K_AP_UNMQR: {
       double *Cbase = t.kind == K_UNMQR ? a.A : a.C;
-      const int cs = t.s * ws, wsz = min(ws, nb - cs);
-      unmqr_strip(tile_ptr(a.A, p, nb, t.i, t.k), tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0),
-                  tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs, wsz, a.trans != 0, 0, nblk, smem, L, mbph, tma);
+      const int cs = t.s * ws;
+      const StripJob J{tile_ptr(a.A, p, nb, t.i, t.k), tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0), nullptr,
+                       tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs, min(ws, nb - cs), 0, nblk, a.trans != 0, false,
+                       mA, t.kind == K_UNMQR ? mA : mC, col(t.i, t.k), 0};
+      strip_update<SU_UN>(J, smem, L, ph);
       break;
     }
     case K_TTMQR:
@@ -984,10 +950,12 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
       const bool ap = t.kind == K_AP_TTMQR || t.kind == K_AP_TSMQR;
       const bool tri = t.kind == K_TTMQR || t.kind == K_AP_TTMQR;
       double *Cbase = ap ? a.C : a.A;
-      const int cs = t.s * ws, wsz = min(ws, nb - cs);
-      tpmqr_strip(tile_ptr(a.A, p, nb, t.i, t.k), tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1),
-                  tile_ptr(Cbase, p, nb, t.piv, t.j), tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs, wsz, tri,
-                  a.trans != 0, 0, nblk, smem, L, mbph, tma);
+      const int cs = t.s * ws;
+      const StripJob J{tile_ptr(a.A, p, nb, t.i, t.k), tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1),
+                       tile_ptr(Cbase, p, nb, t.piv, t.j), tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs,
+                       min(ws, nb - cs), 0, nblk, a.trans != 0, false, mA, ap ? mC : mA, col(t.i, t.k), col(t.piv, t.j)};
+      if (tri) strip_update<SU_TT>(J, smem, L, ph);
+      else strip_update<SU_TS>(J, smem, L, ph);
       break;
     }
     default:
@@ -1063,15 +1031,15 @@ __device__ __forceinline__ bool is_panel_block(int kind) {
   return kind == K_GEQRT_B || kind == K_TTQRT_B || kind == K_TSQRT_B;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) tqr_persistent(const __grid_constant__ RunArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_task, s_chain, s_resident;
   const SmemLayout L = smem_layout(a.nb, a.ib, a.ws);
   if (threadIdx.x == 0) {
-    s_prof_on = 0; s_chain = -1; s_resident = 0; mbar_init();
+    s_prof_on = 0; s_chain = -1; s_resident = 0; mbar_init_all();
     s_epoch = (unsigned)ld_acquire(&a.ctrl[kCtrlEpoch]);
   }
-  unsigned mbph = 0u;   // parity of the CTA mbarrier (identical in every thread)
+  unsigned ph = 0u;     // parity bits of the two buffer mbarriers (identical in every thread)
   // everything the DMMA padding may read must be finite: start from zeros
   for (size_t x = threadIdx.x; x < L.total; x += kThreads) smem[x] = 0.0;
   __syncthreads();
@@ -1127,7 +1095,7 @@ __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(RunArgs a) {
     // while the task runs and are consumed only when releasing
     int2 e0 = make_int2(-1, 0);
     if (threadIdx.x < 32 && tk.dep_begin + (int)threadIdx.x < tk.dep_end) e0 = __ldg(a.succ + tk.dep_begin + threadIdx.x);
-    run_task(a, tk, smem, L, s_resident != 0, mbph);
+    run_task(a, tk, smem, L, s_resident != 0, ph);
     __syncthreads();
     prof_mark(PH_STORE);
     int keep = -1;   // (lane 0) successor this CTA runs next without queueing it

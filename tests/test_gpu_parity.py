@@ -303,14 +303,16 @@ def test_tall_skinny_domains_on_one_gpu(world, tree):
     assert rel(nu.sign_normalise(R), nu.sign_normalise(Rl)) <= TOL_R
 
 
+@pytest.mark.parametrize("tma", ["0", "1"])
 @pytest.mark.parametrize("tree,family", [("greedy", "TT"), ("flat", "TS")])
-def test_tma_bulk_copy_path(tree, family, monkeypatch):
-    """TQR_TMA=1 moves C strips and V blocks with 1-D TMA bulk copies
-    (cp.async.bulk + mbarrier); results equal the oracle as on the default path."""
-    monkeypatch.setenv("TQR_TMA", "1")
-    for (p, q, nb, ib) in [(4, 2, 72, 32), (3, 3, 64, 32), (6, 3, 20, 8)]:
+def test_copy_paths(tree, family, tma, monkeypatch):
+    """Both copy paths of the strip updates: TMA tensor copies (default when nb % 8 == 0,
+    ib % 8 == 0, nb >= 32) and cp.async (TQR_TMA=0, and every other shape) equal the oracle."""
+    monkeypatch.setenv("TQR_TMA", tma)
+    for (p, q, nb, ib) in [(4, 2, 72, 32), (3, 3, 64, 32), (6, 3, 40, 8), (3, 2, 200, 32), (6, 3, 20, 8)]:
         A = qrinputs.gaussian(p * nb, q * nb, 123 + p)
         compare_with_oracle(A, nb, ib, tree, 1, family)
+        assert tq.last_launch_tma() == (tma == "1" and nb % 8 == 0 and ib % 8 == 0 and nb >= 32)
     A = qrinputs.gaussian(8 * 64, 3 * 64, 7)
     compare_with_oracle(A, 64, 32, "plasma", 3, "TT")
 
