@@ -23,6 +23,13 @@ constexpr size_t kMaxSmem = 227 * 1024 - 512;   // dynamic smem budget (opt-in m
 constexpr int kTld = 33;
 constexpr int kLdw = 36;                    // W^T / W2^T in smem: element (col, refl) at col + refl * kLdw
 constexpr int kSlots = 8;                   // row tiles of 8 per warp in a strip update (nb <= 256)
+#ifndef TQR_BOX
+#define TQR_BOX 4
+#endif
+constexpr int kBoxTiles = TQR_BOX;          // row tiles per TMA box of a V block
+#ifndef TQR_EXP
+#define TQR_EXP 0                           // (timing experiments of tools/strip_bench only; 0 in the product)
+#endif
 constexpr int kTraceWords = 13;             // per-task trace record (diagnostics): 4 stamps/ids, 8 phases, push time
 // scheduler control words (ints; each on its own 128-byte line): per priority
 // level l a queue head at kCtrlHead + 64 l, its tail at kCtrlTail + 64 l and
@@ -148,10 +155,10 @@ __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)_
 
 // ---- asynchronous global -> shared copies ------------------------------------
 // cp.async (LDGSTS) with zero fill: `valid` = false writes zeros without a
-// global read. Completion is tracked per buffer by an mbarrier: every thread
-// ends its batch with cp.async.mbarrier.arrive.noinc (the barrier expects one
-// arrival per thread), so consumers wait on the mbarrier instead of a CTA-wide
-// barrier. Writers of a tile are ordered before readers by the release/acquire
+// global read. Completion is tracked per buffer by an mbarrier: the one warp
+// that issues a buffer's copies ends with cp.async.mbarrier.arrive.noinc on
+// every lane (the barrier expects those 32 arrivals, plus the TMA transaction
+// bytes), so consumers wait on the mbarrier instead of a CTA-wide barrier. Writers of a tile are ordered before readers by the release/acquire
 // task counters plus a gpu-scope fence.
 __device__ __forceinline__ void cp_async16_zf(double *dst, const double *src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 16 : 0)
@@ -163,11 +170,13 @@ __device__ __forceinline__ void cp_async8_zf(double *dst, const double *src, boo
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-__shared__ __align__(8) unsigned long long s_mbar[2];   // one per V/T/C1 buffer
+__shared__ __align__(8) unsigned long long s_mbar[2];   // one per V/T/C1 buffer ("full": 32 arrivals of the issuing warp)
+__shared__ int s_done[2];      // warps done with a buffer's block (the 8th refills it)
 
 __device__ __forceinline__ void mbar_init_all() {
   for (int b = 0; b < 2; ++b)
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_mbar[b])), "r"(kThreads) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_mbar[b])), "r"(32) : "memory");
+  s_done[0] = s_done[1] = 0;
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -190,13 +199,13 @@ __device__ __forceinline__ void mbar_wait(int b, unsigned &ph) {
 // rows [row0, row0 + 8 ntl) of columns [c0, c0 + ncol) (ncol <= 32) of the
 // column-major tile X (ld nb) -> row-tile layout dst (tile 0 = rows row0..row0+7);
 // rows outside [0, nb) are zero-filled; columns >= ncol are left untouched.
-// Warp w copies (row tile, 8 columns) chunks: lane -> column lane/4, row pair lane%4.
+// Issued by one warp: per (row tile, 8 columns) chunk, lane -> column lane/4, row pair lane%4.
 __device__ __forceinline__ void load_tiles8(double *dst, const double *X, int nb, int row0, int ntl, int c0,
                                             int ncol) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int cl = lane >> 2, pr = 2 * (lane & 3);
   const bool v16 = ((nb | row0) & 1) == 0;
-  for (int ch = warp; ch < ntl * 4; ch += kWarps) {
+  for (int ch = 0; ch < ntl * 4; ++ch) {
     const int tl = ch >> 2, c = 8 * (ch & 3) + cl;
     if (c < ncol) {
       const int r = row0 + 8 * tl + pr;
@@ -211,14 +220,14 @@ __device__ __forceinline__ void load_tiles8(double *dst, const double *X, int nb
     }
   }
 }
-// T block of inner block j0 (bw columns of a T slot, ld ib) -> dst (same layout)
+// T block of inner block j0 (bw columns of a T slot, ld ib) -> dst (same layout); one warp
 __device__ __forceinline__ void load_tblock(double *dst, const double *Tslot, int ib, int j0, int bw) {
-  const int n = bw * ib;
+  const int n = bw * ib, lane = threadIdx.x & 31;
   const double *s = Tslot + (size_t)j0 * ib;
   if ((ib & 1) == 0) {
-    for (int i = 2 * threadIdx.x; i < n; i += 2 * kThreads) cp_async16_zf(dst + i, s + i, true);
+    for (int i = 2 * lane; i < n; i += 64) cp_async16_zf(dst + i, s + i, true);
   } else {
-    for (int i = threadIdx.x; i < n; i += kThreads) cp_async8_zf(dst + i, s + i, true);
+    for (int i = lane; i < n; i += 32) cp_async8_zf(dst + i, s + i, true);
   }
 }
 
@@ -243,14 +252,6 @@ __device__ __forceinline__ void mbar_expect_tx(int b, unsigned bytes) {
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_mbar[b])), "r"(bytes)
                : "memory");
 }
-// order this thread's earlier generic-proxy accesses (global data published by
-// other SMs and acquired by this CTA; shared-memory writes of this CTA) before
-// its next async-proxy (TMA) copies
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
 // ---- FP64 tensor-core MMA (DMMA): D(16x8) += A(16x4) B(4x8) ------------------
 // Fragments (lane = 4*g + t): a0 = A[g][t], a1 = A[g+8][t]; b0 = B[t][g];
 // d0,d1 = D[g][2t, 2t+1], d2,d3 = D[g+8][2t, 2t+1].
@@ -549,7 +550,8 @@ struct StripJob {
   int nb, ib, cs, wsz;  // strip = columns [cs, cs + wsz) of C1 / C2
   int b_lo, b_hi;       // inner blocks applied (ascending for Q^T, descending for Q)
   bool trans, resident; // resident: block b_lo's V and T are already in buffer 0 (panel chain)
-  const CUtensorMap *mV, *mC;   // TMA path: tensor maps of the V tile's and the C tiles' matrix (null: cp.async)
+  const CUtensorMap *mV, *mC1;  // TMA path: tensor maps (boxes of kBoxTiles / 4 row tiles) of the V tile's and the
+                                // C1 tile's matrix (null: cp.async)
   int vcol, c1col;              // global column of the V tile's and the C1 tile's first column
 };
 
@@ -569,30 +571,36 @@ __device__ __forceinline__ double vmask(double v, int r, int l, int j0) {
   return r <= j0 + l ? v : 0.0;
 }
 
-// copies of block b into buffer `buf` (all threads; one mbarrier arrival each);
-// vt = false: V and T are already there (panel chain), only the C1 window moves
+// copies of block b into buffer `buf`, issued by ONE warp (32 mbarrier
+// arrivals); vt = false: V and T are already there (panel chain), only the C1
+// window moves
 template <int KIND>
 __device__ __forceinline__ void su_issue(const StripJob &J, const SmemLayout &L, double *smem, int buf, int b,
                                          bool vt = true) {
+  const int lane = threadIdx.x & 31;
   const int j0 = b * J.ib, bw = min(J.ib, J.nb - j0);
   int lo, hi;
   su_range<KIND>(j0, bw, L.ntile, lo, hi);
   if (J.mV) {
-    // one thread issues: V as 4-tile boxes ending at row tile hi (a box never
-    // leaves [0, ntile): ntile >= 4 on this path), T as one bulk copy, the C1
-    // window as one 4-tile box at row tile j0/8 (j0 % 8 == 0 on this path)
-    if (threadIdx.x == 0) {
-      fence_proxy_async();
-      const int nv = vt ? (hi - lo + 3) >> 2 : 0;
-      const unsigned tbytes = vt ? (unsigned)(bw * J.ib) * 8u : 0u;
-      mbar_expect_tx(buf, (unsigned)nv * 8192u + tbytes + (KIND != SU_UN ? 8192u : 0u));
-      double *V = smem + L.offV[buf];
-      for (int e = hi, x = 0; x < nv; ++x, e -= 4) {
-        const int st = e - 4 > 0 ? e - 4 : 0;
-        tma_box(V + st * 256, J.mV, J.vcol + j0, st, buf);
-      }
-      if (vt) tma_bulk(smem + L.offT[buf], J.Tslot + (size_t)j0 * J.ib, tbytes, buf);
-      if (KIND != SU_UN) tma_box(smem + L.offC1[buf], J.mC, J.c1col + J.cs, j0 >> 3, buf);
+    // one copy per lane: V as boxes of kBoxTiles row tiles ending at row tile
+    // hi (lanes 0..; a box never leaves [0, ntile): ntile >= 4 on this path),
+    // T as one bulk copy (lane 30), the C1 window as one 4-tile box at row
+    // tile j0/8 (lane 31; j0 % 8 == 0 on this path)
+    const int nv = vt ? (hi - lo + kBoxTiles - 1) / kBoxTiles : 0;
+    const unsigned tbytes = vt ? (unsigned)(bw * J.ib) * 8u : 0u;
+    if (lane == 0)
+      mbar_expect_tx(buf, (unsigned)nv * (2048u * kBoxTiles) + tbytes + (KIND != SU_UN ? 8192u : 0u));
+    // generic -> async proxy ordering: global data acquired from other SMs,
+    // this CTA's shared-memory writes (masked band tiles of earlier blocks)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (lane < nv) {
+      const int e = hi - kBoxTiles * lane, st = e - kBoxTiles > 0 ? e - kBoxTiles : 0;
+      tma_box(smem + L.offV[buf] + st * 256, J.mV, J.vcol + j0, st, buf);
+    } else if (lane == 30 && vt) {
+      tma_bulk(smem + L.offT[buf], J.Tslot + (size_t)j0 * J.ib, tbytes, buf);
+    } else if (lane == 31 && KIND != SU_UN) {
+      tma_box(smem + L.offC1[buf], J.mC1, J.c1col + J.cs, j0 >> 3, buf);
     }
   } else {
     if (vt) {
@@ -634,7 +642,7 @@ __device__ __forceinline__ void su_p1(const double (&acc)[kSlots][4], double (&w
     for (int nn = 0; nn < 4; ++nn) bv[nn] = *reinterpret_cast<const double2 *>(vt + 64 * nn);
     // the band tiles (<= 5, crossing the block's diagonal) are always among
     // the last two active slots: mask them here and store the masked tile back
-    // (column half 0's warp) so phase 3 reads a clean V
+    // (both column groups store the same values) so phase 3 reads a clean V
     if (KIND != SU_TS && s + 2 >= N && j < band_hi && j >= band_lo) {
       const int r = 8 * j + 2 * t;
 #pragma unroll
@@ -679,11 +687,18 @@ __device__ __forceinline__ void su_p3(double (&acc)[kSlots][4], const double (&w
     case 7: CALL(7); break; case 8: CALL(8); break; default: break;                         \
   }
 
+__device__ __forceinline__ void group_sync(int id) {   // named barrier of one 4-warp column group
+  asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
+}
+
 template <int KIND>
 __device__ void strip_update(const StripJob &J, double *smem, const SmemLayout &L, unsigned &ph) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
-  const int rg = warp >> 1, mh = warp & 1, cg = 16 * mh + g;
-  const int mt = warp & 1, nt = warp >> 1;            // phase-2 fragment of this warp
+  // two independent column groups (warps 0-3: columns 0-15, warps 4-7:
+  // columns 16-31), one warp per SM sub-partition each, synchronised only by
+  // their own named barriers: one group's latency-bound steps (reduction,
+  // phase 2, copy issue) overlap the other group's DMMA phases
+  const int mh = warp >> 2, rg = warp & 3, cg = 16 * mh + g, gbar = 1 + mh;
   const int nb = J.nb, ib = J.ib, ntile = L.ntile, wsz = J.wsz;
   const int nblk = J.b_hi - J.b_lo;
   const bool even = (nb & 1) == 0;
@@ -691,8 +706,13 @@ __device__ void strip_update(const StripJob &J, double *smem, const SmemLayout &
   if (KIND == SU_UN) ct_lo = (J.b_lo * ib) >> 3;
   if (KIND == SU_TT) ct_hi = (min(J.b_hi * ib, nb) + 7) >> 3;
   const int ntask = su_nact<KIND>(rg, ct_lo, ct_hi, ntile);   // slots holding C rows of this task
+  const bool active = 16 * mh < wsz;                  // a column group beyond a narrow strip idles
   const bool wait0 = !J.resident || KIND != SU_UN;     // resident TT/TS blocks still load their C1 window
-  if (wait0) su_issue<KIND>(J, L, smem, 0, J.trans ? J.b_lo : J.b_hi - 1, !J.resident);
+  auto blk = [&](int idx) { return J.trans ? J.b_lo + idx : J.b_hi - 1 - idx; };
+  if (warp == 0) {                                    // both buffers are free: blocks 0 and 1
+    if (wait0) su_issue<KIND>(J, L, smem, 0, blk(0), !J.resident);
+    if (nblk > 1) su_issue<KIND>(J, L, smem, 1, blk(1));
+  }
 
   // C strip -> registers: acc[s] = C^T fragment (columns cg, cg+8; rows 8j+2t, 8j+2t+1)
   double acc[kSlots][4];
@@ -721,21 +741,21 @@ __device__ void strip_update(const StripJob &J, double *smem, const SmemLayout &
 
   for (int idx = 0; idx < nblk; ++idx) {
     const int cur = idx & 1;
-    const int b = J.trans ? J.b_lo + idx : J.b_hi - 1 - idx;
+    const int b = blk(idx);
     const int j0 = b * ib, bw = min(ib, nb - j0);
     int blo, bhi;
     su_range<KIND>(j0, bw, ntile, blo, bhi);
-    const int nact = 16 * mh < wsz ? su_nact<KIND>(rg, blo, bhi, ntile) : 0;   // (a column half beyond a narrow strip idles)
+    const int nact = active ? su_nact<KIND>(rg, blo, bhi, ntile) : 0;
     const int band_lo = j0 >> 3, band_hi = (j0 + bw + 7) >> 3;   // tiles crossing the block's diagonal
     if (idx > 0 || wait0) mbar_wait(cur, ph);
-    prof_mark(PH_LOAD);
+    prof_mark(idx == 0 ? PH_LOAD : PH_PANEL);   // (tracer: first copy wait vs later ones)
     double *Vb = smem + L.offV[cur];
     const double *Tb = smem + L.offT[cur], *C1w = smem + L.offC1[cur];
     // phase-2 B operand: op(T)^T fragments of this warp's n-tile (T upper triangular, zero-padded)
     double tb[8];
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
-      const int r = J.trans ? 4 * kk + t : 8 * nt + g, c = J.trans ? 8 * nt + g : 4 * kk + t;
+      const int r = J.trans ? 4 * kk + t : 8 * rg + g, c = J.trans ? 8 * rg + g : 4 * kk + t;
       tb[kk] = (r <= c && c < bw) ? Tb[r + c * ib] : 0.0;
     }
 
@@ -745,8 +765,10 @@ __device__ void strip_update(const StripJob &J, double *smem, const SmemLayout &
     for (int nn = 0; nn < 4; ++nn)
 #pragma unroll
       for (int e = 0; e < 4; ++e) wacc[nn][e] = 0.0;
-#define TQR_P1(N) su_p1<KIND, N>(acc, wacc, Vb, rg, ntile, j0, band_lo, band_hi, mh == 0)
-    TQR_SLOT_SWITCH(nact, TQR_P1)
+#define TQR_P1(N) su_p1<KIND, N>(acc, wacc, Vb, rg, ntile, j0, band_lo, band_hi, true)
+    for (int rep = 0; rep < ((TQR_EXP & 32) ? 4 : 1); ++rep) {
+      TQR_SLOT_SWITCH(nact, TQR_P1)
+    }
 #undef TQR_P1
     {
       double *Wp = smem + L.offWp + rg * 32 * kLdw;
@@ -759,53 +781,43 @@ __device__ void strip_update(const StripJob &J, double *smem, const SmemLayout &
         Wp[cg + 8 + (rf + 1) * kLdw] = wacc[nn][3];
       }
     }
-    __syncthreads();
+    group_sync(gbar);
     prof_mark(PH_MMA1);
-    // the other buffer is free now (its last reader was the previous block's phase 3)
-    if (idx + 1 < nblk) su_issue<KIND>(J, L, smem, cur ^ 1, J.trans ? b + 1 : b - 1);
 
-    // ---- reduce the 4 partials (+ the C1 window: identity part of V)
+    // ---- phase 2: W2^T fragment (columns 16 mh.., reflectors 8 rg..) = -W^T op(T)^T,
+    // W^T = the group's 4 partials (+ the C1 window: identity part of V), summed
+    // while loading the A fragments
     {
-      double *W = smem + L.offW;
       const double *Wp0 = smem + L.offWp;
-      const int r8 = lane & 7, c4 = lane >> 3;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int x = warp * 4 + i, rt = x >> 3, cb = x & 7;
-        const int refl = 8 * rt + r8, col = 4 * cb + c4, o = col + refl * kLdw;
-        double v = (Wp0[o] + Wp0[o + 32 * kLdw]) + (Wp0[o + 64 * kLdw] + Wp0[o + 96 * kLdw]);
-        if (KIND != SU_UN) v += C1w[rt * 256 + col * 8 + r8];
-        W[o] = v;
-      }
-    }
-    __syncthreads();
-    prof_mark(PH_FIX);
-
-    // ---- phase 2: W2^T fragment (columns 16 mt.., reflectors 8 nt..) = -W^T op(T)^T
-    {
-      const double *W = smem + L.offW;
       double *W2 = smem + L.offW2;
       double a2[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
-        const double a0 = W[(16 * mt + g) + (4 * kk + t) * kLdw];
-        const double a1 = W[(16 * mt + g + 8) + (4 * kk + t) * kLdw];
+        const int o0 = (16 * mh + g) + (4 * kk + t) * kLdw, o1 = o0 + 8;
+        double a0 = (Wp0[o0] + Wp0[o0 + 32 * kLdw]) + (Wp0[o0 + 64 * kLdw] + Wp0[o0 + 96 * kLdw]);
+        double a1 = (Wp0[o1] + Wp0[o1 + 32 * kLdw]) + (Wp0[o1 + 64 * kLdw] + Wp0[o1 + 96 * kLdw]);
+        if (KIND != SU_UN) {   // C1_b[refl 4kk+t][col]: row-tile layout of the window
+          const int rf = 4 * kk + t;
+          a0 += C1w[(rf >> 3) * 256 + (16 * mh + g) * 8 + (rf & 7)];
+          a1 += C1w[(rf >> 3) * 256 + (16 * mh + g + 8) * 8 + (rf & 7)];
+        }
         dmma(a2[kk & 1], a0, a1, tb[kk]);
       }
+      prof_mark(PH_FIX);
       double w2[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) w2[e] = -(a2[0][e] + a2[1][e]);
-      const int rf = 8 * nt + 2 * t;
-      W2[(16 * mt + g) + rf * kLdw] = w2[0];
-      W2[(16 * mt + g) + (rf + 1) * kLdw] = w2[1];
-      W2[(16 * mt + g + 8) + rf * kLdw] = w2[2];
-      W2[(16 * mt + g + 8) + (rf + 1) * kLdw] = w2[3];
+      const int rf = 8 * rg + 2 * t;
+      W2[(16 * mh + g) + rf * kLdw] = w2[0];
+      W2[(16 * mh + g) + (rf + 1) * kLdw] = w2[1];
+      W2[(16 * mh + g + 8) + rf * kLdw] = w2[2];
+      W2[(16 * mh + g + 8) + (rf + 1) * kLdw] = w2[3];
       if (KIND != SU_UN) {   // C1_b rows j0 + rf, rf + 1 += W2 (straight to global)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int col = 16 * mt + g + 8 * h;
+          const int col = 16 * mh + g + 8 * h;
           if (col < wsz && rf < bw) {
-            const double2 c1 = *reinterpret_cast<const double2 *>(C1w + nt * 256 + col * 8 + 2 * t);
+            const double2 c1 = *reinterpret_cast<const double2 *>(C1w + rg * 256 + col * 8 + 2 * t);
             double *dst = J.C1 + (j0 + rf) + (size_t)(J.cs + col) * nb;
             const double v0 = c1.x + w2[2 * h], v1 = c1.y + w2[2 * h + 1];
             if (rf + 1 < bw && ((nb | j0) & 1) == 0) {
@@ -818,7 +830,7 @@ __device__ void strip_update(const StripJob &J, double *smem, const SmemLayout &
         }
       }
     }
-    __syncthreads();
+    group_sync(gbar);
     prof_mark(PH_TRI);
 
     // ---- phase 3: C^T += W2^T V^T on this warp's row tiles
@@ -831,10 +843,22 @@ __device__ void strip_update(const StripJob &J, double *smem, const SmemLayout &
         wa1[kk] = W2[cg + 8 + (4 * kk + t) * kLdw];
       }
 #define TQR_P3(N) su_p3<KIND, N>(acc, wa0, wa1, Vb, rg, ntile)
-      TQR_SLOT_SWITCH(nact, TQR_P3)
+      for (int rep = 0; rep < ((TQR_EXP & 64) ? 4 : 1); ++rep) {
+        TQR_SLOT_SWITCH(nact, TQR_P3)
+      }
 #undef TQR_P3
     }
     prof_mark(PH_MMA3);
+    // this warp is done with buffer `cur`; the 8th warp to finish refills it with block idx + 2
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      __threadfence_block();
+      last = atomicAdd(&s_done[cur], 1) == kWarps - 1;
+      if (last) s_done[cur] = 0;
+      __threadfence_block();
+    }
+    if (__shfl_sync(0xffffffffu, last, 0) && idx + 2 < nblk) su_issue<KIND>(J, L, smem, cur, blk(idx + 2));
   }
 
   // ---- C strip back to global (only the rows and columns this task owns)
@@ -1032,7 +1056,7 @@ __device__ __forceinline__ bool is_panel_block(int kind) {
 }
 
 __global__ void __launch_bounds__(kThreads, 1) tqr_persistent(const __grid_constant__ RunArgs a) {
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];   // (TMA tensor copies need 128-byte-aligned destinations)
   __shared__ int s_task, s_chain, s_resident;
   const SmemLayout L = smem_layout(a.nb, a.ib, a.ws);
   if (threadIdx.x == 0) {
