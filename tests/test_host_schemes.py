@@ -125,3 +125,31 @@ def test_bad_arguments_raise():
     with pytest.raises(tq.TiledQRError):
         tq.critical_path(5, 2, 9)
     assert "p >= q" in tq.lib().tqr_last_error().decode() or tq.lib().tqr_last_error()
+
+
+def _oracle_des(args):
+    """Oracle critical path and tiled zeroing times of one (tree, family) case (worker process)."""
+    p, q, tree, bs, family = args
+    tasks = dag.expand(schemes.elim_list(tree, p, q, bs), p, q, family)
+    _, fin = dag.simulate(tasks)
+    return max(fin), dag.zero_times(tasks, fin)
+
+
+def test_configs4_large_des_matches_oracle():
+    """configs[4]: the product's critical_path and tiled_times (C++ DES of the Algorithm 2/3
+    expansion, §3) equal the oracle DES bit for bit at (p, q) =
+    (1000, 100), (1000, 1) and (333, 77), for every tree and both kernel families. The oracle
+    needs ~35 s and 2.5 GB per (1000, 100) case, so the cases run in a 4-process pool."""
+    from concurrent.futures import ProcessPoolExecutor
+    import multiprocessing as mp
+    trees = [("flat", 1), ("fibonacci", 1), ("greedy", 1), ("binary", 1), ("plasma", 10)]
+    cases = [(p, q, tree, bs, fam) for (p, q) in [(1000, 100), (333, 77), (1000, 1)]
+             for tree, bs in trees for fam in ("TT", "TS")]
+    with ProcessPoolExecutor(max_workers=4, mp_context=mp.get_context("spawn")) as ex:
+        results = list(ex.map(_oracle_des, cases))
+    for (p, q, tree, bs, fam), (cp, zt) in zip(cases, results):
+        assert tq.critical_path(p, q, tree, bs, fam) == cp, (p, q, tree, bs, fam)
+        got_cp, z = tq.tiled_times(p, q, tree, bs, fam)
+        assert got_cp == cp
+        assert {(i, k): int(z[i - 1, k - 1]) for (i, k) in zt} == zt, (p, q, tree, bs, fam)
+        assert int(np.count_nonzero(z)) == len(zt)
