@@ -104,3 +104,76 @@ def test_gloo_tall_skinny_reduction(world, tree):
     R = np.triu(result["R"])
     assert np.linalg.norm(nu.sign_normalise(R) - nu.sign_normalise(Ru)) / np.linalg.norm(Ru) < 1e-12
     assert result["merges0"] == (world - 1).bit_length()
+
+
+class _OracleQ:
+    """Test-only factor handle: the oracle's Factor (its taus replay Q)."""
+
+    def __init__(self, F):
+        self.F = F
+
+
+def oracle_factor_q(A, m, n, nb, ib, tree, bs, family):
+    p, q = m // nb, n // nb
+    lst = merge_list(q) if tree == "merge" else schemes.elim_list(tree, p, q, bs)
+    F = nu.tiled_qr(qrinputs.from_tiles(A.numpy(), p, q, nb), nb, ib, lst, family)
+    A.copy_(torch.from_numpy(qrinputs.to_tiles(F.A, nb)))
+    return _OracleQ(F)
+
+
+def oracle_apply(A, H, C, m, n, nb, ib, tree, bs, family, trans):
+    """Test-only apply backend: the oracle's apply_qt / apply_q on the tiled C, in place."""
+    p = m // nb
+    qc = C.numel() // (m * nb)
+    dense = qrinputs.from_tiles(C.numpy(), p, qc, nb)
+    out = (nu.apply_qt if trans else nu.apply_q)(H.F, dense)
+    C.copy_(torch.from_numpy(qrinputs.to_tiles(np.asfortranarray(out), nb)))
+
+
+def _apply_worker(rank, world, port, p, q, qc, nb, ib, tree, result):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = qrinputs.gaussian(p * nb, q * nb, 41)
+        B = np.asfortranarray(np.hstack([A, qrinputs.gaussian(p * nb, (qc - q) * nb, 42)]))
+        r0, r1 = tdist.domain(p, world, rank)
+        A_loc = torch.from_numpy(qrinputs.to_tiles(np.asfortranarray(A[r0 * nb:r1 * nb]), nb))
+        B_loc = torch.from_numpy(qrinputs.to_tiles(np.asfortranarray(B[r0 * nb:r1 * nb]), nb))
+        F = tdist.tall_skinny_qr(A_loc, p, q, nb, ib, tree, 1, "TT", factor=oracle_factor_q)
+        tdist.apply_qt(F, B_loc, qc * nb, apply=oracle_apply)
+        result[f"qtb{rank}"] = qrinputs.from_tiles(B_loc.numpy(), r1 - r0, qc, nb)
+        if rank == 0:
+            result["R"] = qrinputs.from_tiles(F.R.numpy(), q, q, nb)
+        tdist.apply_q(F, B_loc, qc * nb, apply=oracle_apply)
+        result[f"back{rank}"] = qrinputs.from_tiles(B_loc.numpy(), r1 - r0, qc, nb)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,tree", [(2, "greedy"), (3, "flat"), (4, "fibonacci")])
+def test_gloo_distributed_apply(world, tree):
+    """Q^T and Q of the distributed factor (local factors + merge tree) over gloo:
+    Q^T [A | X] puts R in rank 0's top tile rows and zeros below it for the A
+    columns (A = QR), preserves column norms (Q orthogonal),
+    solves least squares (R x = (Q^T b)[:n] equals numpy's lstsq), and Q undoes Q^T."""
+    p, q, qc, nb, ib = 9, 2, 3, 6, 3
+    mgr = mp.Manager()
+    result = mgr.dict()
+    mp.spawn(_apply_worker, args=(world, _free_port(), p, q, qc, nb, ib, tree, result), nprocs=world, join=True)
+    A = qrinputs.gaussian(p * nb, q * nb, 41)
+    B = np.hstack([A, qrinputs.gaussian(p * nb, (qc - q) * nb, 42)])
+    QtB = np.vstack([result[f"qtb{r}"] for r in range(world)])
+    # rows of Q^T B in the order of the distributed Q: rank 0's top q tile rows are (Q^T B)[:n]
+    n = q * nb
+    R = np.triu(result["R"])
+    top = QtB[:n]
+    assert np.linalg.norm(top[:, :n] - R) <= 1e-12 * np.linalg.norm(R)
+    rest = np.vstack([QtB[n:]])
+    assert np.linalg.norm(rest[:, :n]) <= 1e-12 * np.linalg.norm(A)
+    assert np.allclose(np.linalg.norm(QtB, axis=0), np.linalg.norm(B, axis=0), rtol=1e-12)
+    x = np.linalg.solve(R, top[:, n:])
+    x_ref = np.linalg.lstsq(A, B[:, n:], rcond=None)[0]
+    assert np.linalg.norm(x - x_ref) <= 1e-10 * np.linalg.norm(x_ref)
+    back = np.vstack([result[f"back{r}"] for r in range(world)])
+    assert np.linalg.norm(back - B) <= 1e-12 * np.linalg.norm(B)

@@ -462,3 +462,82 @@ def test_graph_replay_and_oversized_grid(monkeypatch):
     monkeypatch.setenv("TQR_GRID", str(4 * torch.cuda.get_device_properties(0).multi_processor_count))
     buf2, T2 = run_gpu(A, nb, ib, "greedy", 1, "TT")
     assert rel(qrinputs.from_tiles(buf2.cpu().numpy(), p, q, nb), F.A) <= TOL_R
+
+
+class _Mailbox:
+    """In-process stand-in for torch.distributed point-to-point (tests only):
+    rank threads exchange tensors through queues; every kernel is launched on
+    the one default stream, so no kernel ever waits on another."""
+
+    def __init__(self, world):
+        import queue
+        self.world = world
+        self.q = {(s, d): queue.Queue() for s in range(world) for d in range(world)}
+
+    def endpoint(self, rank):
+        box = self
+
+        class _End:
+            world = box.world
+
+            def __init__(self):
+                self.rank = rank
+
+            def send(self, t, dst):
+                torch.cuda.synchronize()
+                box.q[(rank, dst)].put(t.clone())
+
+            def recv(self, t, src):
+                t.copy_(box.q[(src, rank)].get(timeout=120))
+                torch.cuda.synchronize()
+        return _End()
+
+
+@pytest.mark.parametrize("world,tree", [(2, "greedy"), (3, "fibonacci"), (4, "flat")])
+def test_distributed_apply_threads(world, tree):
+    """dist.tall_skinny_qr + dist.apply_qt / apply_q with the CUDA kernels, the ranks
+    run as threads on one GPU (mailbox exchange): Q^T [A | X] gives R on top and
+    zeros below it for the A columns, least squares matches numpy, Q undoes Q^T."""
+    import threading
+    from paper_1104_4475_b200 import dist as tdist
+    p, q, qc, nb, ib = 10, 2, 3, 64, 32
+    n = q * nb
+    A = qrinputs.gaussian(p * nb, n, 77)
+    B = np.asfortranarray(np.hstack([A, qrinputs.gaussian(p * nb, (qc - q) * nb, 78)]))
+    box = _Mailbox(world)
+    out, errs = {}, []
+
+    def run(rank):
+        try:
+            r0, r1 = tdist.domain(p, world, rank)
+            A_loc = torch.from_numpy(qrinputs.to_tiles(np.asfortranarray(A[r0 * nb:r1 * nb]), nb)).to(DEV)
+            B_loc = torch.from_numpy(qrinputs.to_tiles(np.asfortranarray(B[r0 * nb:r1 * nb]), nb)).to(DEV)
+            comm = box.endpoint(rank)
+            F = tdist.tall_skinny_qr(A_loc, p, q, nb, ib, tree, 1, "TT", comm=comm)
+            tdist.apply_qt(F, B_loc, qc * nb, comm=comm)
+            torch.cuda.synchronize()
+            out[f"qtb{rank}"] = qrinputs.from_tiles(B_loc.cpu().numpy(), r1 - r0, qc, nb)
+            if rank == 0:
+                out["R"] = qrinputs.from_tiles(F.R.cpu().numpy(), q, q, nb)
+            tdist.apply_q(F, B_loc, qc * nb, comm=comm)
+            torch.cuda.synchronize()
+            out[f"back{rank}"] = qrinputs.from_tiles(B_loc.cpu().numpy(), r1 - r0, qc, nb)
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    ths = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(300)
+    assert not errs, errs
+    QtB = np.vstack([out[f"qtb{r}"] for r in range(world)])
+    R = np.triu(out["R"])
+    assert np.linalg.norm(QtB[:n, :n] - R) <= 1e-12 * np.linalg.norm(R)
+    assert np.linalg.norm(QtB[n:, :n]) <= 1e-12 * np.linalg.norm(A)
+    assert np.allclose(np.linalg.norm(QtB, axis=0), np.linalg.norm(B, axis=0), rtol=1e-12)
+    x = np.linalg.solve(R, QtB[:n, n:])
+    x_ref = np.linalg.lstsq(A, B[:, n:], rcond=None)[0]
+    assert np.linalg.norm(x - x_ref) <= 1e-10 * np.linalg.norm(x_ref)
+    back = np.vstack([out[f"back{r}"] for r in range(world)])
+    assert np.linalg.norm(back - B) <= 1e-12 * np.linalg.norm(B)
