@@ -58,12 +58,14 @@ class TiledQRError(RuntimeError):
 
 
 def lib():
-    """Load libtiledqr.so (built in-tree by __graft_entry__.build()). Raises if absent."""
+    """Load libtiledqr.so (built in-tree by __graft_entry__.build()). Raises if absent.
+    TQR_LIB names another in-tree build of the same library (A/B timing of kernel variants)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise TiledQRError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
-        L = ctypes.CDLL(LIB_PATH)
+        path = os.environ.get("TQR_LIB") or LIB_PATH
+        if not os.path.exists(path):
+            raise TiledQRError(f"{path} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(path)
         for name, (res, args) in _SIGS.items():
             f = getattr(L, name)
             f.restype = res

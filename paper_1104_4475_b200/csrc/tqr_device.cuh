@@ -28,7 +28,8 @@ constexpr int kSlots = 8;                   // row tiles of 8 per warp in a stri
 #endif
 constexpr int kBoxTiles = TQR_BOX;          // row tiles per TMA box of a V block
 #ifndef TQR_EXP
-#define TQR_EXP 0                           // (timing experiments of tools/strip_bench only; 0 in the product)
+#define TQR_EXP 0                           // (timing experiments of tools/strip_bench only; 0 in the product:
+                                            //  32/64 repeat phase 1/3, 128/256 drop phase 1/3's V loads)
 #endif
 constexpr int kTraceWords = 13;             // per-task trace record (diagnostics): 4 stamps/ids, 8 phases, push time
 // scheduler control words (ints; each on its own 128-byte line): per priority
@@ -639,7 +640,7 @@ __device__ __forceinline__ void su_p1(const double (&acc)[kSlots][4], double (&w
     double *vt = Vb + j * 256 + g * 8 + 2 * t;
     double2 bv[4];
 #pragma unroll
-    for (int nn = 0; nn < 4; ++nn) bv[nn] = *reinterpret_cast<const double2 *>(vt + 64 * nn);
+    for (int nn = 0; nn < 4; ++nn) bv[nn] = *reinterpret_cast<const double2 *>(vt + 64 * ((TQR_EXP & 128) ? 0 : nn));
     // the band tiles (<= 5, crossing the block's diagonal) are always among
     // the last two active slots: mask them here and store the masked tile back
     // (both column groups store the same values) so phase 3 reads a clean V
@@ -673,7 +674,7 @@ __device__ __forceinline__ void su_p3(double (&acc)[kSlots][4], const double (&w
 #pragma unroll
     for (int s = 0; s < N; ++s) {
       const int j = su_tile<KIND>(rg, s, ntile);
-      bb[s] = Vb[j * 256 + (4 * kk + t) * 8 + g];
+      bb[s] = Vb[j * 256 + (4 * ((TQR_EXP & 256) ? 0 : kk) + t) * 8 + g];
     }
 #pragma unroll
     for (int s = 0; s < N; ++s) dmma(acc[s], wa0[kk], wa1[kk], bb[s]);
@@ -698,7 +699,10 @@ __device__ void strip_update(const StripJob &J, double *smem, const SmemLayout &
   // columns 16-31), one warp per SM sub-partition each, synchronised only by
   // their own named barriers: one group's latency-bound steps (reduction,
   // phase 2, copy issue) overlap the other group's DMMA phases
-  const int mh = warp >> 2, rg = warp & 3, cg = 16 * mh + g, gbar = 1 + mh;
+  // the row groups of column group 1 are rotated by one against group 0's, so
+  // the row group with an extra row tile (n_tiles % 4 != 0) lands on two
+  // different sub-partitions (warp w runs on sub-partition w % 4)
+  const int mh = warp >> 2, rg = (warp + mh) & 3, cg = 16 * mh + g, gbar = 1 + mh;
   const int nb = J.nb, ib = J.ib, ntile = L.ntile, wsz = J.wsz;
   const int nblk = J.b_hi - J.b_lo;
   const bool even = (nb & 1) == 0;
