@@ -224,9 +224,10 @@ def trace_graph(ntask: int):
 
 
 def plan_graph(m: int, n: int, nb: int, ib: int = 32, tree="greedy", bs: int = 1, family="TT", ws: int = 0,
-               split: bool = True):
-    """Host-only diagnostic: the device task graph (tasks[ntask, 8], succ_ptr, succ)."""
-    args = (m, n, nb, ib, _tree(tree), bs, _fam(family), ws, 1 if split else 0)
+               split: bool = True, mstrip: int = 0):
+    """Host-only diagnostic: the device task graph (tasks[ntask, 8], succ_ptr, succ).
+    tasks[:, 5] = strip | (strips of the task << 16); mstrip = strips per update task (0: the default)."""
+    args = (m, n, nb, ib, _tree(tree), bs, _fam(family), ws, (1 if split else 0) | (mstrip << 8))
     nt = _check(lib().tqr_plan_graph(*args, None, 0, None, None, 0))
     tasks = np.zeros(8 * nt, np.int32)
     ptr = np.zeros(nt + 1, np.int32)

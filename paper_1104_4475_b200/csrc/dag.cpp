@@ -202,7 +202,8 @@ DevTask mk(int kind, int i, int piv, int k, int j, int s) {
 }  // namespace
 
 void build_factor_graph(const std::vector<TileTask> &tt, const std::vector<int64_t> &start,
-                        int p, int q, int nb, int ws, bool split_panels, DevGraph &g) {
+                        int p, int q, int nb, int ws, bool split_panels, DevGraph &g, int mstrip) {
+  if (mstrip < 1) mstrip = 1;
   const int S = (nb + ws - 1) / ws;
   g.tasks.clear();
   std::vector<std::vector<int>> deps;
@@ -292,11 +293,14 @@ void build_factor_graph(const std::vector<TileTask> &tt, const std::vector<int64
         const std::vector<int> *src = nullptr;
         for (int d : t.deps)
           if (tt[d].kind == K_GEQRT && tt[d].i == t.i && tt[d].k == t.k) src = &panel_dev[d];
-        for (int s = 0; s < S; ++s) {
+        for (int s = 0; s < S; s += mstrip) {   // one task per mstrip consecutive strips
+          const int ns = std::min(mstrip, S - s);
           dl.assign(src->begin(), src->end());
-          push_lw(i, j, s);
-          int id = add(mk(K_UNMQR, i, 0, k, j, s), dl, start[x]);
-          lw[slot(i, j, s)] = id;
+          for (int u = 0; u < ns; ++u) push_lw(i, j, s + u);
+          DevTask m = mk(K_UNMQR, i, 0, k, j, s);
+          m.pad = ns;
+          int id = add(m, dl, start[x]);
+          for (int u = 0; u < ns; ++u) lw[slot(i, j, s + u)] = id;
         }
         break;
       }
@@ -305,12 +309,14 @@ void build_factor_graph(const std::vector<TileTask> &tt, const std::vector<int64
         const int qk = t.kind == K_TTMQR ? K_TTQRT : K_TSQRT;
         for (int d : t.deps)
           if (tt[d].kind == qk && tt[d].i == t.i && tt[d].k == t.k) src = &panel_dev[d];
-        for (int s = 0; s < S; ++s) {
+        for (int s = 0; s < S; s += mstrip) {
+          const int ns = std::min(mstrip, S - s);
           dl.assign(src->begin(), src->end());
-          push_lw(pv, j, s);
-          push_lw(i, j, s);
-          int id = add(mk(t.kind, i, pv, k, j, s), dl, start[x]);
-          lw[slot(pv, j, s)] = lw[slot(i, j, s)] = id;
+          for (int u = 0; u < ns; ++u) { push_lw(pv, j, s + u); push_lw(i, j, s + u); }
+          DevTask m = mk(t.kind, i, pv, k, j, s);
+          m.pad = ns;
+          int id = add(m, dl, start[x]);
+          for (int u = 0; u < ns; ++u) lw[slot(pv, j, s + u)] = lw[slot(i, j, s + u)] = id;
         }
         break;
       }
@@ -364,7 +370,7 @@ void build_apply_graph(const std::vector<TileTask> &tt, int p, int qc, int nb, i
 
 // Relative task durations for the bottom-level priorities (microseconds of the
 // B200 kernels on nb = 200 tiles, from the per-task tracer; only the ratios matter).
-static double est_duration(int kind) {
+static double est_kind_duration(int kind) {
   switch (kind) {
     case K_GEQRT_B: case K_TTQRT_B: return 71;
     case K_TSQRT_B: return 80;
@@ -377,6 +383,10 @@ static double est_duration(int kind) {
     case K_TSQRT: return 500;
     default: return 40;
   }
+}
+
+static double est_duration(const DevTask &t) {   // multi-strip update tasks run their strips in turn
+  return est_kind_duration(t.kind) * (t.pad > 1 ? t.pad : 1);
 }
 
 // Non-preemptive list scheduling on nproc identical processors: whenever a
@@ -401,7 +411,7 @@ static double list_schedule(const DevGraph &g, const std::vector<int32_t> &cnt, 
       const int t = ready.top().second;
       ready.pop();
       start[t] = now;
-      running.emplace(now + est_duration(g.tasks[t].kind), t);
+      running.emplace(now + est_duration(g.tasks[t]), t);
       --free;
     }
     if (running.empty()) break;
@@ -442,13 +452,13 @@ void finalize_dataflow(DevGraph &g, bool lookahead, int levels, int prio_rule, i
   for (int t = n - 1; t >= 0; --t) {
     double m = 0.0;
     for (int x = cnt[t]; x < cnt[t + 1]; ++x) m = std::max(m, bl[g.succ[x]]);
-    bl[t] = est_duration(g.tasks[t].kind) + m;
+    bl[t] = est_duration(g.tasks[t]) + m;
     blmax = std::max(blmax, bl[t]);
   }
   // ASAP start of every task with the same estimates (tasks are in topological order)
   std::vector<double> asap(n, 0.0);
   for (int t = 0; t < n; ++t) {
-    const double f = asap[t] + est_duration(g.tasks[t].kind);
+    const double f = asap[t] + est_duration(g.tasks[t]);
     for (int x = cnt[t]; x < cnt[t + 1]; ++x) asap[g.succ[x]] = std::max(asap[g.succ[x]], f);
   }
   // priority key: 0 = bottom level; 1 = earliest ASAP start first; 2 = bottom level

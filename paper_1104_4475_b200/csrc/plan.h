@@ -56,7 +56,7 @@ struct DevTask {
   int32_t dep_begin, dep_end;
   int32_t meta;
   int32_t chain;
-  int32_t pad;
+  int32_t pad;                     // update tasks of other tiles: number of strips (>= 1), else 0
 };
 static_assert(sizeof(DevTask) == 32, "DevTask layout");
 
@@ -80,8 +80,10 @@ void finalize_dataflow(DevGraph &g, bool prioritize = true, int levels = kLevels
 // ceil(nb/ws) column strips of width ws; with split_panels (requires ws == ib)
 // every panel kernel becomes per-inner-block panel tasks plus trailing strip
 // tasks.
+// Update tasks of other tiles (UNMQR / TTMQR / TSMQR) cover mstrip consecutive
+// strips each (DevTask::pad = their count), run one after another by one CTA.
 void build_factor_graph(const std::vector<TileTask> &tt, const std::vector<int64_t> &start,
-                        int p, int q, int nb, int ws, bool split_panels, DevGraph &g);
+                        int p, int q, int nb, int ws, bool split_panels, DevGraph &g, int mstrip = 1);
 
 // Apply graph for C (p x qc tiles): Q^T (trans=1) or Q (trans=0).
 void build_apply_graph(const std::vector<TileTask> &tt, int p, int qc, int nb, int ws,

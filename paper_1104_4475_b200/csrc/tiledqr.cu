@@ -109,6 +109,12 @@ static int pick_ws(int nb, int ib) {
 
 static int check_shape(int m, int n, int nb, int ib, int &p, int &q);
 
+// strips per update task of the factorization (TQR_MSTRIP, default 2)
+static int mstrip_default() {
+  const int m = env_int("TQR_MSTRIP", 2);
+  return m < 1 ? 1 : (m > 8 ? 8 : m);
+}
+
 // ---- plan cache -------------------------------------------------------------
 struct DevPlan {
   DevTask *tasks = nullptr;
@@ -180,7 +186,7 @@ static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, in
                                 std::to_string(smem_bytes(nb, ib, ws)) + " bytes of shared memory for nb = " +
                                 std::to_string(nb) + "; at most " + std::to_string(kMaxSmem) + " fit");
   PlanKey key{dev, mode, p, q, qc, nb, ib, tree, bs, family,
-              (ws * 4 + (env_int("TQR_SPLIT", 1) != 0) * 2 + (env_int("TQR_LOOKAHEAD", 1) != 0)) * 64 +
+              65536 * mstrip_default() + (ws * 4 + (env_int("TQR_SPLIT", 1) != 0) * 2 + (env_int("TQR_LOOKAHEAD", 1) != 0)) * 64 +
                   env_int("TQR_LEVELS", kLevels) + 4096 * env_int("TQR_PRIO", 0)};
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_plans.find(key);
@@ -192,7 +198,7 @@ static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, in
   if (rc < 0) return rc;
   DevGraph g;
   const bool split = env_int("TQR_SPLIT", 1) != 0 && ws == ib && nb > ib;
-  if (mode == 0) build_factor_graph(tt, st, p, q, nb, ws, split, g);
+  if (mode == 0) build_factor_graph(tt, st, p, q, nb, ws, split, g, mstrip_default());
   else build_apply_graph(tt, p, qc, nb, ws, mode == 1, g);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -222,7 +228,8 @@ extern "C" int64_t tqr_plan_graph(int m, int n, int nb, int ib, int tree, int bs
   rc = tile_sim(p, q, tree, bs, family, tt, st, fin, mk);
   if (rc < 0) return rc;
   DevGraph g;
-  build_factor_graph(tt, st, p, q, nb, ws, split != 0 && ws == ib && nb > ib, g);
+  const int ms = (split >> 8) > 0 ? (split >> 8) : mstrip_default();
+  build_factor_graph(tt, st, p, q, nb, ws, (split & 1) != 0 && ws == ib && nb > ib, g, ms);
   finalize_dataflow(g, true, kLevels, 0, 148);
   const int64_t nt = (int64_t)g.tasks.size();
   if (!out_tasks || !succ_ptr || !succ) return nt;          // size query
@@ -230,7 +237,8 @@ extern "C" int64_t tqr_plan_graph(int m, int n, int nb, int ib, int tree, int bs
   for (int64_t t = 0; t < nt; ++t) {
     const DevTask &d = g.tasks[t];
     int32_t *o = out_tasks + 8 * t;
-    o[0] = d.kind; o[1] = d.i; o[2] = d.piv; o[3] = d.k; o[4] = d.j; o[5] = d.s; o[6] = d.chain; o[7] = d.meta;
+    o[0] = d.kind; o[1] = d.i; o[2] = d.piv; o[3] = d.k; o[4] = d.j; o[6] = d.chain; o[7] = d.meta;
+    o[5] = d.s | ((d.pad > 1 ? d.pad : 1) << 16);   // strip | strip count << 16
     succ_ptr[t] = d.dep_begin;
   }
   succ_ptr[nt] = (int32_t)g.succ.size();

@@ -127,8 +127,11 @@ __shared__ unsigned long long s_prof[8];
 __shared__ unsigned long long s_prof_last;
 __shared__ int s_prof_on;
 enum { PH_LOAD = 0, PH_FIX, PH_MMA1, PH_TRI, PH_MMA3, PH_PANEL, PH_TREC, PH_STORE };
+#ifndef TQR_PROF
+#define TQR_PROF 0                          // 1: in-task phase counters for the tracer (costs ~4% in the hot loops)
+#endif
 __device__ __forceinline__ void prof_mark(int slot) {
-  if (threadIdx.x == 0 && s_prof_on) {
+  if (TQR_PROF && threadIdx.x == 0 && s_prof_on) {
     unsigned long long now = clock64();
     s_prof[slot] += now - s_prof_last;
     s_prof_last = now;
@@ -964,11 +967,14 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
     case K_UNMQR:
     case K_AP_UNMQR: {
       double *Cbase = t.kind == K_UNMQR ? a.A : a.C;
-      const int cs = t.s * ws;
-      const StripJob J{tile_ptr(a.A, p, nb, t.i, t.k), tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0), nullptr,
-                       tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs, min(ws, nb - cs), 0, nblk, a.trans != 0, false,
-                       mA, t.kind == K_UNMQR ? mA : mC, col(t.i, t.k), 0};
-      strip_update<SU_UN>(J, smem, L, ph);
+      for (int u = 0; u < max(t.pad, 1); ++u) {   // (multi-strip task: its strips in turn)
+        if (u > 0) __syncthreads();
+        const int cs = (t.s + u) * ws;
+        const StripJob J{tile_ptr(a.A, p, nb, t.i, t.k), tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0), nullptr,
+                         tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs, min(ws, nb - cs), 0, nblk, a.trans != 0, false,
+                         mA, t.kind == K_UNMQR ? mA : mC, col(t.i, t.k), 0};
+        strip_update<SU_UN>(J, smem, L, ph);
+      }
       break;
     }
     case K_TTMQR:
@@ -978,12 +984,16 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
       const bool ap = t.kind == K_AP_TTMQR || t.kind == K_AP_TSMQR;
       const bool tri = t.kind == K_TTMQR || t.kind == K_AP_TTMQR;
       double *Cbase = ap ? a.C : a.A;
-      const int cs = t.s * ws;
-      const StripJob J{tile_ptr(a.A, p, nb, t.i, t.k), tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1),
-                       tile_ptr(Cbase, p, nb, t.piv, t.j), tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs,
-                       min(ws, nb - cs), 0, nblk, a.trans != 0, false, mA, ap ? mC : mA, col(t.i, t.k), col(t.piv, t.j)};
-      if (tri) strip_update<SU_TT>(J, smem, L, ph);
-      else strip_update<SU_TS>(J, smem, L, ph);
+      for (int u = 0; u < max(t.pad, 1); ++u) {
+        if (u > 0) __syncthreads();
+        const int cs = (t.s + u) * ws;
+        const StripJob J{tile_ptr(a.A, p, nb, t.i, t.k), tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1),
+                         tile_ptr(Cbase, p, nb, t.piv, t.j), tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs,
+                         min(ws, nb - cs), 0, nblk, a.trans != 0, false, mA, ap ? mC : mA, col(t.i, t.k),
+                         col(t.piv, t.j)};
+        if (tri) strip_update<SU_TT>(J, smem, L, ph);
+        else strip_update<SU_TS>(J, smem, L, ph);
+      }
       break;
     }
     default:

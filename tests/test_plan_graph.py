@@ -33,6 +33,7 @@ def reach(ptr, succ):
 def writes(t, nb, ib, ws):
     """(tile, strip) slots a task writes; strips are ws columns wide."""
     kind, i, piv, k, j, s = (int(x) for x in t[:6])
+    s, ns = s & 0xffff, max(s >> 16, 1)        # multi-strip update tasks: strips s .. s + ns - 1
     name = tq.KIND_NAMES[kind]
     strips_of_block = lambda b: {(b * ib) // ws}
     if name in ("GEQRT_B",):
@@ -44,9 +45,9 @@ def writes(t, nb, ib, ws):
     if name in ("TTQRT_U", "TSQRT_U"):
         return {((i, k), s), ((piv, k), s)}
     if name == "UNMQR":
-        return {((i, j), s)}
+        return {((i, j), s + u) for u in range(ns)}
     if name in ("TTMQR", "TSMQR"):
-        return {((i, j), s), ((piv, j), s)}
+        return {((i, j), s + u) for u in range(ns)} | {((piv, j), s + u) for u in range(ns)}
     if name == "GEQRT":
         return {((i, k), x) for x in range(-(-nb // ws))}
     if name in ("TTQRT", "TSQRT"):
@@ -59,10 +60,11 @@ CASES = [("greedy", 1, "TT"), ("flat", 1, "TS"), ("fibonacci", 1, "TT"), ("binar
 
 
 @pytest.mark.parametrize("tree,bs,family", CASES)
-@pytest.mark.parametrize("p,q,nb,split", [(6, 3, 72, True), (5, 2, 64, True), (4, 4, 64, False)])
-def test_plan_graph_invariants(tree, bs, family, p, q, nb, split):
+@pytest.mark.parametrize("p,q,nb,split,mstrip", [(6, 3, 72, True, 1), (6, 3, 72, True, 2), (5, 2, 64, True, 2),
+                                                  (4, 4, 64, False, 1), (4, 3, 200, True, 3)])
+def test_plan_graph_invariants(tree, bs, family, p, q, nb, split, mstrip):
     ib = ws = 32
-    tasks, ptr, succ = tq.plan_graph(p * nb, q * nb, nb, ib, tree, bs, family, ws, split)
+    tasks, ptr, succ = tq.plan_graph(p * nb, q * nb, nb, ib, tree, bs, family, ws, split, mstrip)
     n = len(tasks)
     # topological priority order and indegrees
     indeg = np.zeros(n, np.int64)
@@ -103,7 +105,7 @@ def test_plan_graph_invariants(tree, bs, family, p, q, nb, split):
         if src is None:
             continue
         need = panel_of[src] if name in ("UNMQR", "TTMQR", "TSMQR") else [
-            u for u in panel_of[src] if int(tasks[u, 5]) == int(tasks[t, 4])]
+            u for u in panel_of[src] if int(tasks[u, 5]) & 0xFFFF == int(tasks[t, 4])]
         for u in need:
             assert (r[u] >> t) & 1, (name, src)
     # task counts from the tile-level DAG
@@ -113,7 +115,7 @@ def test_plan_graph_invariants(tree, bs, family, p, q, nb, split):
     expect = 0
     for tt in tiles:
         if tt.kind in ("UNMQR", "TTMQR", "TSMQR"):
-            expect += S
+            expect += -(-S // mstrip)
         elif split and nb > ib:
             expect += nblk + nblk * (nblk - 1) // 2
         else:
