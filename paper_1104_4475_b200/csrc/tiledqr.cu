@@ -109,9 +109,10 @@ static int pick_ws(int nb, int ib) {
 
 static int check_shape(int m, int n, int nb, int ib, int &p, int &q);
 
-// strips per update task of the factorization (TQR_MSTRIP, default 2)
-static int mstrip_default() {
-  const int m = env_int("TQR_MSTRIP", 2);
+// strips per update task of the factorization (TQR_MSTRIP; default 3 when q >= 20,
+// where parallelism is ample, else 2: profiles/r02_experiments_session3.txt item 10)
+static int mstrip_default(int q) {
+  const int m = env_int("TQR_MSTRIP", q >= 20 ? 3 : 2);
   return m < 1 ? 1 : (m > 8 ? 8 : m);
 }
 
@@ -186,7 +187,7 @@ static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, in
                                 std::to_string(smem_bytes(nb, ib, ws)) + " bytes of shared memory for nb = " +
                                 std::to_string(nb) + "; at most " + std::to_string(kMaxSmem) + " fit");
   PlanKey key{dev, mode, p, q, qc, nb, ib, tree, bs, family,
-              65536 * mstrip_default() + (ws * 4 + (env_int("TQR_SPLIT", 1) != 0) * 2 + (env_int("TQR_LOOKAHEAD", 1) != 0)) * 64 +
+              65536 * mstrip_default(q) + (ws * 4 + (env_int("TQR_SPLIT", 1) != 0) * 2 + (env_int("TQR_LOOKAHEAD", 1) != 0)) * 64 +
                   env_int("TQR_LEVELS", kLevels) + 4096 * env_int("TQR_PRIO", 0)};
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_plans.find(key);
@@ -198,7 +199,7 @@ static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, in
   if (rc < 0) return rc;
   DevGraph g;
   const bool split = env_int("TQR_SPLIT", 1) != 0 && ws == ib && nb > ib;
-  if (mode == 0) build_factor_graph(tt, st, p, q, nb, ws, split, g, mstrip_default());
+  if (mode == 0) build_factor_graph(tt, st, p, q, nb, ws, split, g, mstrip_default(q));
   else build_apply_graph(tt, p, qc, nb, ws, mode == 1, g);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -228,7 +229,7 @@ extern "C" int64_t tqr_plan_graph(int m, int n, int nb, int ib, int tree, int bs
   rc = tile_sim(p, q, tree, bs, family, tt, st, fin, mk);
   if (rc < 0) return rc;
   DevGraph g;
-  const int ms = (split >> 8) > 0 ? (split >> 8) : mstrip_default();
+  const int ms = (split >> 8) > 0 ? (split >> 8) : mstrip_default(q);
   build_factor_graph(tt, st, p, q, nb, ws, (split & 1) != 0 && ws == ib && nb > ib, g, ms);
   finalize_dataflow(g, true, kLevels, 0, 148);
   const int64_t nt = (int64_t)g.tasks.size();

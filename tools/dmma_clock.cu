@@ -26,18 +26,19 @@ __global__ void k(double *out, unsigned long long *o, int iters, double x) {
 int main() {
   double *out; unsigned long long *o, h[2];
   cudaMalloc(&out, 8 * 148 * 1024); cudaMalloc(&o, 16);
+  for (int grid : {1, 2, 8, 37, 74, 111, 148})
   for (int thr : {128, 256}) {
-    int iters = 200000;
-    k<<<148, thr>>>(out, o, 1000, 1.0);
+    int iters = 100000;
+    k<<<grid, thr>>>(out, o, 1000, 1.0);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    k<<<148, thr>>>(out, o, iters, 1.0);
+    k<<<grid, thr>>>(out, o, iters, 1.0);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     cudaMemcpy(h, o, 16, cudaMemcpyDeviceToHost);
-    double dm = 8.0 * iters * (thr / 32) * 148;
-    printf("threads %d: %.2f TFLOP/s  cycles %llu  ns %llu  => SM clock %.0f MHz, %.2f cycles/DMMA/SMSP\n", thr,
-           dm * 1024 / (ms * 1e-3) / 1e12, h[0], h[1], 1e3 * h[0] / (double)h[1],
+    double dm = 8.0 * iters * (thr / 32) * grid;
+    printf("grid %3d threads %d: %.2f TFLOP/s  cycles %llu  ns %llu  => SM clock %.0f MHz, %.2f cycles/DMMA/SMSP\n", thr,
+           grid, dm * 1024 / (ms * 1e-3) / 1e12, h[0], h[1], 1e3 * h[0] / (double)h[1],
            (double)h[0] / (8.0 * iters * (thr / 32) / 4));
   }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
