@@ -541,3 +541,26 @@ def test_distributed_apply_threads(world, tree):
     assert np.linalg.norm(x - x_ref) <= 1e-10 * np.linalg.norm(x_ref)
     back = np.vstack([out[f"back{r}"] for r in range(world)])
     assert np.linalg.norm(back - B) <= 1e-12 * np.linalg.norm(B)
+
+
+def test_concurrent_kernel_on_another_stream():
+    """A long kernel holding SMs on another stream (an fp64 GEMM issued just
+    before) does not stall the factorization: the first CTA to arrive seeds the
+    roots, so the dataflow progresses with whatever CTAs are resident, and the
+    result equals the oracle's."""
+    p, q, nb, ib = 6, 3, 64, 32
+    m, n = p * nb, q * nb
+    A = qrinputs.gaussian(m, n, 23)
+    F = nu.tiled_qr(A, nb, ib, schemes.elim_list("greedy", p, q), "TT")
+    X = torch.randn(6144, 6144, dtype=torch.float64, device=DEV)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    buf = torch.from_numpy(qrinputs.to_tiles(A, nb)).to(DEV)
+    T = torch.zeros(tq.t_size(m, n, nb, ib), dtype=torch.float64, device=DEV)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        Y = X @ X
+    with torch.cuda.stream(s2):
+        tq.tiled_qr(buf, m, n, nb, ib, "greedy", T=T, stream=s2)
+    torch.cuda.synchronize()
+    assert torch.isfinite(Y).all()
+    assert rel(qrinputs.from_tiles(buf.cpu().numpy(), p, q, nb), F.A) <= TOL_R
