@@ -46,13 +46,21 @@ __global__ void __launch_bounds__(256, 1) k(const __grid_constant__ Args a) {
       __syncthreads();
     } else {
       if (threadIdx.x == 0) {
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su(&mbar)), "r"(200 * 32 * 8 + (a.mode == 0 ? 3 * 2048 : 0)));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su(&mbar)), "r"(a.mode == 5 ? 102400 : 200 * 32 * 8 + (a.mode == 0 ? 3 * 2048 : 0)));
         if (a.mode == 0) {
           for (int e = 25, x = 0; x < 7; ++x, e -= 4) {
             const int st = e - 4 > 0 ? e - 4 : 0;
             asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
                          ::"r"(su(sm + st * 256)), "l"(&a.m3d4), "r"(0), "r"((int)col0 + cs), "r"(st), "r"(su(&mbar)) : "memory");
           }
+        } else if (a.mode == 4) {   // one 1-D bulk copy of the contiguous 51200-byte block
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(su(sm)), "l"(a.A + col0 * nb + (size_t)cs * nb), "r"(51200), "r"(su(&mbar)) : "memory");
+        } else if (a.mode == 5) {   // two 1-D bulk copies (V and Y of a block)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(su(sm)), "l"(a.A + col0 * nb + (size_t)cs * nb), "r"(51200), "r"(su(&mbar)) : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(su(sm + 6400)), "l"(a.A + col0 * nb + (size_t)cs * nb + 40000), "r"(51200), "r"(su(&mbar)) : "memory");
         } else if (a.mode == 1) {
           asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
                        ::"r"(su(sm)), "l"(&a.m3d25), "r"(0), "r"((int)col0 + cs), "r"(0), "r"(su(&mbar)) : "memory");
@@ -96,13 +104,13 @@ int main() {
         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   a.A = A; a.out = o; a.reps = 200;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  const char *nm[4] = {"3d4 (7 boxes)", "3d25 (1 box) ", "2d (1 box)   ", "cp.async     "};
-  for (int mode = 0; mode < 4; ++mode)
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+  const char *nm[6] = {"3d4 (7 boxes)", "3d25 (1 box) ", "2d (1 box)   ", "cp.async     ", "1d bulk 51KB ", "2x1d bulk    "};
+  for (int mode = 0; mode < 6; ++mode)
     for (int nc : {1, ncta}) {
       a.mode = mode;
-      k<<<nc, 256, 100 * 1024>>>(a);
-      k<<<nc, 256, 100 * 1024>>>(a);
+      k<<<nc, 256, 110 * 1024>>>(a);
+      k<<<nc, 256, 110 * 1024>>>(a);
       cudaMemcpy(&h, o, 8, cudaMemcpyDeviceToHost);
       printf("%s ctas=%3d: %6llu cycles per 200x32 block (%.1f B/cycle/SM)\n", nm[mode], nc, h, 51200.0 / h);
     }
