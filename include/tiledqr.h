@@ -168,7 +168,9 @@ int64_t tqr_trace_fetch(uint64_t *out, int64_t cap);
 int64_t tqr_trace_graph(int32_t *succ_ptr, int32_t *succ, int64_t cap);
 
 /* Diagnostics, host only (no GPU): the device task graph tiled_qr would run
- * (strip width ws, 0 = default; split = per-inner-block panel tasks). Fills
+ * (strip width ws, 0 = default; split bit 0 = per-inner-block panel tasks,
+ * bit 1 / bit 2 = UNMQR+TTMQR fusion on / off (neither: TQR_FUSE, default off),
+ * bits 8.. = strips per update task, 0 = default). Fills
  * out_tasks with 8 int32 per task (kind, i, piv, k, j, s, chain, meta) in
  * priority order and the successor CSR (succ_ptr[ntask+1], succ). With null
  * outputs it only returns the task count. Returns ntask or a TQR_E* code. */

@@ -191,7 +191,7 @@ def trace_enable(on: bool = True):
 
 
 KIND_NAMES = ["GEQRT", "UNMQR", "TTQRT", "TTMQR", "TSQRT", "TSMQR", "AP_UNMQR", "AP_TTMQR", "AP_TSMQR",
-              "GEQRT_B", "GEQRT_U", "TTQRT_B", "TTQRT_U", "TSQRT_B", "TSQRT_U"]
+              "GEQRT_B", "GEQRT_U", "TTQRT_B", "TTQRT_U", "TSQRT_B", "TSQRT_U", "UNTTMQR"]
 
 
 PHASES = ["load", "fix", "mma1", "tri", "mma3", "panel", "trec", "store"]
@@ -224,10 +224,12 @@ def trace_graph(ntask: int):
 
 
 def plan_graph(m: int, n: int, nb: int, ib: int = 32, tree="greedy", bs: int = 1, family="TT", ws: int = 0,
-               split: bool = True, mstrip: int = 0):
+               split: bool = True, mstrip: int = 0, fuse=None):
     """Host-only diagnostic: the device task graph (tasks[ntask, 8], succ_ptr, succ).
-    tasks[:, 5] = strip | (strips of the task << 16); mstrip = strips per update task (0: the default)."""
-    args = (m, n, nb, ib, _tree(tree), bs, _fam(family), ws, (1 if split else 0) | (mstrip << 8))
+    tasks[:, 5] = strip | (strips of the task << 16); mstrip = strips per update task (0: the default);
+    fuse = UNMQR + TTMQR fusion (None: the library default, TQR_FUSE)."""
+    fz = 0 if fuse is None else (2 if fuse else 4)
+    args = (m, n, nb, ib, _tree(tree), bs, _fam(family), ws, (1 if split else 0) | fz | (mstrip << 8))
     nt = _check(lib().tqr_plan_graph(*args, None, 0, None, None, 0))
     tasks = np.zeros(8 * nt, np.int32)
     ptr = np.zeros(nt + 1, np.int32)

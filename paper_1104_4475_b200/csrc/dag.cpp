@@ -15,6 +15,7 @@
 // does not block a later writer (the reflectors and the rewritten part of the
 // tile are disjoint).
 #include <algorithm>
+#include <map>
 #include <numeric>
 #include <queue>
 #include "plan.h"
@@ -202,8 +203,39 @@ DevTask mk(int kind, int i, int piv, int k, int j, int s) {
 }  // namespace
 
 void build_factor_graph(const std::vector<TileTask> &tt, const std::vector<int64_t> &start,
-                        int p, int q, int nb, int ws, bool split_panels, DevGraph &g, int mstrip) {
+                        int p, int q, int nb, int ws, bool split_panels, DevGraph &g, int mstrip, bool fuse) {
   if (mstrip < 1) mstrip = 1;
+  // Fusion (TT family): an UNMQR(i, k, j) whose next task on tile (i, j) (in
+  // emission order, i.e. its only successor on that tile) is the
+  // TTMQR(i, piv, k, j) eliminating the same row is not emitted; the TTMQR's
+  // device tasks become K_UNTTMQR tasks that run both on each strip. Nothing
+  // else touches tile (i, j) in between, so the strip's history is unchanged.
+  std::vector<int> fused_from(tt.size(), -1);
+  if (fuse) {
+    std::map<std::pair<int, int>, int> last;   // tile -> last tile task touching it
+    auto touch = [&](int r, int c, int x) {
+      auto it = last.find({r, c});
+      if (it != last.end()) {
+        const TileTask &u = tt[it->second], &y = tt[x];
+        if (u.kind == K_UNMQR && y.kind == K_TTMQR && y.i == u.i && y.k == u.k && y.j == u.j && r == y.i)
+          fused_from[x] = it->second;
+      }
+      last[{r, c}] = x;
+    };
+    for (size_t x = 0; x < tt.size(); ++x) {
+      const TileTask &t = tt[x];
+      switch (t.kind) {
+        case K_GEQRT: touch(t.i, t.k, (int)x); break;
+        case K_UNMQR: touch(t.i, t.j, (int)x); break;
+        case K_TTQRT: case K_TSQRT: touch(t.i, t.k, (int)x); touch(t.piv, t.k, (int)x); break;
+        case K_TTMQR: case K_TSMQR: touch(t.i, t.j, (int)x); touch(t.piv, t.j, (int)x); break;
+        default: break;
+      }
+    }
+  }
+  std::vector<char> skip(tt.size(), 0);
+  for (size_t x = 0; x < tt.size(); ++x)
+    if (fused_from[x] >= 0) skip[fused_from[x]] = 1;
   const int S = (nb + ws - 1) / ws;
   g.tasks.clear();
   std::vector<std::vector<int>> deps;
@@ -289,6 +321,7 @@ void build_factor_graph(const std::vector<TileTask> &tt, const std::vector<int64
         break;
       }
       case K_UNMQR: {
+        if (skip[x]) break;   // runs inside the fused task of its TTMQR
         // the reflector source is the GEQRT of tile (i,k): the unique dep with kind GEQRT on (i,k)
         const std::vector<int> *src = nullptr;
         for (int d : t.deps)
@@ -309,11 +342,16 @@ void build_factor_graph(const std::vector<TileTask> &tt, const std::vector<int64
         const int qk = t.kind == K_TTMQR ? K_TTQRT : K_TSQRT;
         for (int d : t.deps)
           if (tt[d].kind == qk && tt[d].i == t.i && tt[d].k == t.k) src = &panel_dev[d];
+        const std::vector<int> *usrc = nullptr;   // fused: the UNMQR's reflector source, GEQRT(i, k)
+        if (fused_from[x] >= 0)
+          for (int d : tt[fused_from[x]].deps)
+            if (tt[d].kind == K_GEQRT && tt[d].i == t.i && tt[d].k == t.k) usrc = &panel_dev[d];
         for (int s = 0; s < S; s += mstrip) {
           const int ns = std::min(mstrip, S - s);
           dl.assign(src->begin(), src->end());
+          if (usrc) dl.insert(dl.end(), usrc->begin(), usrc->end());
           for (int u = 0; u < ns; ++u) { push_lw(pv, j, s + u); push_lw(i, j, s + u); }
-          DevTask m = mk(t.kind, i, pv, k, j, s);
+          DevTask m = mk(usrc ? K_UNTTMQR : t.kind, i, pv, k, j, s);
           m.pad = ns;
           int id = add(m, dl, start[x]);
           for (int u = 0; u < ns; ++u) lw[slot(pv, j, s + u)] = lw[slot(i, j, s + u)] = id;
@@ -377,6 +415,7 @@ static double est_kind_duration(int kind) {
     case K_GEQRT_U: case K_TTQRT_U: case K_TSQRT_U: return 10;
     case K_UNMQR: case K_AP_UNMQR: return 40;
     case K_TTMQR: case K_AP_TTMQR: return 52;
+    case K_UNTTMQR: return 84;
     case K_TSMQR: case K_AP_TSMQR: return 64;
     case K_GEQRT: return 450;
     case K_TTQRT: return 430;

@@ -17,7 +17,10 @@ enum Kind : int {
   K_AP_UNMQR = 6, K_AP_TTMQR = 7, K_AP_TSMQR = 8,
   // split panel kinds: one inner block b of a panel kernel (s = b), and the
   // update of strip s of the same tile(s) by block b (j = b)
-  K_GEQRT_B = 9, K_GEQRT_U = 10, K_TTQRT_B = 11, K_TTQRT_U = 12, K_TSQRT_B = 13, K_TSQRT_U = 14
+  K_GEQRT_B = 9, K_GEQRT_U = 10, K_TTQRT_B = 11, K_TTQRT_U = 12, K_TSQRT_B = 13, K_TSQRT_U = 14,
+  // factorization only: UNMQR(i, k, j) fused with the TTMQR(i, piv, k, j) that
+  // follows it on tile (i, j) (TT family; one task, the strip stays in registers)
+  K_UNTTMQR = 15
 };
 
 int kind_weight(int kind);   // Table 1 weights in units of nb^3/3
@@ -82,8 +85,10 @@ void finalize_dataflow(DevGraph &g, bool prioritize = true, int levels = kLevels
 // tasks.
 // Update tasks of other tiles (UNMQR / TTMQR / TSMQR) cover mstrip consecutive
 // strips each (DevTask::pad = their count), run one after another by one CTA.
+// fuse: UNMQR + TTMQR pairs on the same tile become K_UNTTMQR tasks.
 void build_factor_graph(const std::vector<TileTask> &tt, const std::vector<int64_t> &start,
-                        int p, int q, int nb, int ws, bool split_panels, DevGraph &g, int mstrip = 1);
+                        int p, int q, int nb, int ws, bool split_panels, DevGraph &g, int mstrip = 1,
+                        bool fuse = false);
 
 // Apply graph for C (p x qc tiles): Q^T (trans=1) or Q (trans=0).
 void build_apply_graph(const std::vector<TileTask> &tt, int p, int qc, int nb, int ws,

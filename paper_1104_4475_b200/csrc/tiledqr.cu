@@ -116,6 +116,11 @@ static int mstrip_default(int q) {
   return m < 1 ? 1 : (m > 8 ? 8 : m);
 }
 
+// UNMQR + TTMQR fusion of the factorization graph (TQR_FUSE=1; off by default:
+// delaying each UNMQR until its row's TTQRT is done costs more than the saved
+// strip load/store and claim, profiles/r02_experiments_session4.txt item 2)
+static bool fuse_default() { return env_int("TQR_FUSE", 0) != 0; }
+
 // ---- plan cache -------------------------------------------------------------
 struct DevPlan {
   DevTask *tasks = nullptr;
@@ -187,7 +192,7 @@ static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, in
                                 std::to_string(smem_bytes(nb, ib, ws)) + " bytes of shared memory for nb = " +
                                 std::to_string(nb) + "; at most " + std::to_string(kMaxSmem) + " fit");
   PlanKey key{dev, mode, p, q, qc, nb, ib, tree, bs, family,
-              65536 * mstrip_default(q) + (ws * 4 + (env_int("TQR_SPLIT", 1) != 0) * 2 + (env_int("TQR_LOOKAHEAD", 1) != 0)) * 64 +
+              (1 << 24) * (int)fuse_default() + 65536 * mstrip_default(q) + (ws * 4 + (env_int("TQR_SPLIT", 1) != 0) * 2 + (env_int("TQR_LOOKAHEAD", 1) != 0)) * 64 +
                   env_int("TQR_LEVELS", kLevels) + 4096 * env_int("TQR_PRIO", 0)};
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_plans.find(key);
@@ -199,7 +204,7 @@ static int get_plan(int mode, int p, int q, int qc, int nb, int ib, int tree, in
   if (rc < 0) return rc;
   DevGraph g;
   const bool split = env_int("TQR_SPLIT", 1) != 0 && ws == ib && nb > ib;
-  if (mode == 0) build_factor_graph(tt, st, p, q, nb, ws, split, g, mstrip_default(q));
+  if (mode == 0) build_factor_graph(tt, st, p, q, nb, ws, split, g, mstrip_default(q), fuse_default());
   else build_apply_graph(tt, p, qc, nb, ws, mode == 1, g);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -230,7 +235,9 @@ extern "C" int64_t tqr_plan_graph(int m, int n, int nb, int ib, int tree, int bs
   if (rc < 0) return rc;
   DevGraph g;
   const int ms = (split >> 8) > 0 ? (split >> 8) : mstrip_default(q);
-  build_factor_graph(tt, st, p, q, nb, ws, (split & 1) != 0 && ws == ib && nb > ib, g, ms);
+  // split bit 1: fusion on, bit 2: fusion off, neither: the default (TQR_FUSE)
+  const bool fuse = (split & 2) ? true : ((split & 4) ? false : fuse_default());
+  build_factor_graph(tt, st, p, q, nb, ws, (split & 1) != 0 && ws == ib && nb > ib, g, ms, fuse);
   finalize_dataflow(g, true, kLevels, 0, 148);
   const int64_t nt = (int64_t)g.tasks.size();
   if (!out_tasks || !succ_ptr || !succ) return nt;          // size query

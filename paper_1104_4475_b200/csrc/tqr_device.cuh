@@ -695,34 +695,14 @@ __device__ __forceinline__ void group_sync(int id) {   // named barrier of one 4
   asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
 }
 
+// C strip <-> registers: acc[s] = C^T fragment of row tile su_tile(rg, s)
+// (columns cg, cg+8; rows 8j+2t, 8j+2t+1); only the first `ntask` slots hold
+// rows of this task
 template <int KIND>
-__device__ void strip_update(const StripJob &J, double *smem, const SmemLayout &L, unsigned &ph) {
+__device__ __forceinline__ void su_load_c(const StripJob &J, double (&acc)[kSlots][4], int rg, int ntask, int ntile) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
-  // two independent column groups (warps 0-3: columns 0-15, warps 4-7:
-  // columns 16-31), one warp per SM sub-partition each, synchronised only by
-  // their own named barriers: one group's latency-bound steps (reduction,
-  // phase 2, copy issue) overlap the other group's DMMA phases
-  // the row groups of column group 1 are rotated by one against group 0's, so
-  // the row group with an extra row tile (n_tiles % 4 != 0) lands on two
-  // different sub-partitions (warp w runs on sub-partition w % 4)
-  const int mh = warp >> 2, rg = (warp + mh) & 3, cg = 16 * mh + g, gbar = 1 + mh;
-  const int nb = J.nb, ib = J.ib, ntile = L.ntile, wsz = J.wsz;
-  const int nblk = J.b_hi - J.b_lo;
+  const int cg = 16 * (warp >> 2) + g, nb = J.nb, wsz = J.wsz;
   const bool even = (nb & 1) == 0;
-  int ct_lo = 0, ct_hi = ntile;                       // row tiles of C this task touches
-  if (KIND == SU_UN) ct_lo = (J.b_lo * ib) >> 3;
-  if (KIND == SU_TT) ct_hi = (min(J.b_hi * ib, nb) + 7) >> 3;
-  const int ntask = su_nact<KIND>(rg, ct_lo, ct_hi, ntile);   // slots holding C rows of this task
-  const bool active = 16 * mh < wsz;                  // a column group beyond a narrow strip idles
-  const bool wait0 = !J.resident || KIND != SU_UN;     // resident TT/TS blocks still load their C1 window
-  auto blk = [&](int idx) { return J.trans ? J.b_lo + idx : J.b_hi - 1 - idx; };
-  if (warp == 0) {                                    // both buffers are free: blocks 0 and 1
-    if (wait0) su_issue<KIND>(J, L, smem, 0, blk(0), !J.resident);
-    if (nblk > 1) su_issue<KIND>(J, L, smem, 1, blk(1));
-  }
-
-  // C strip -> registers: acc[s] = C^T fragment (columns cg, cg+8; rows 8j+2t, 8j+2t+1)
-  double acc[kSlots][4];
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) {
     const int j = su_tile<KIND>(rg, s, ntile), r = 8 * j + 2 * t;
@@ -745,9 +725,49 @@ __device__ void strip_update(const StripJob &J, double *smem, const SmemLayout &
       acc[s][2 * h + 1] = x1;
     }
   }
+}
+template <int KIND>
+__device__ __forceinline__ void su_store_c(const StripJob &J, const double (&acc)[kSlots][4], int rg, int ntask,
+                                           int ntile) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int cg = 16 * (warp >> 2) + g, nb = J.nb, wsz = J.wsz;
+  const bool even = (nb & 1) == 0;
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) {
+    const int j = su_tile<KIND>(rg, s, ntile), r = 8 * j + 2 * t;
+    const bool act = s < ntask && r < nb;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int col = cg + 8 * h;
+      if (act && col < wsz) {
+        double *dst = J.C2 + r + (size_t)(J.cs + col) * nb;
+        if (even) {
+          *reinterpret_cast<double2 *>(dst) = make_double2(acc[s][2 * h], acc[s][2 * h + 1]);
+        } else {
+          dst[0] = acc[s][2 * h];
+          if (r + 1 < nb) dst[1] = acc[s][2 * h + 1];
+        }
+      }
+    }
+  }
+}
+
+// The block loop of one strip job. Block idx uses buffer (base + idx) & 1; the
+// copies of the first two blocks were issued by the caller. The 8th warp done
+// with a buffer refills it with block idx + 2, or, past the job's last block,
+// with the blocks of the next job JN (a TT job: fused UNMQR + TTMQR tasks).
+template <int KIND>
+__device__ __forceinline__ void su_loop(const StripJob &J, const StripJob *JN, double *smem, const SmemLayout &L,
+                                        unsigned &ph, double (&acc)[kSlots][4], int rg, int base, bool wait0) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int mh = warp >> 2, cg = 16 * mh + g, gbar = 1 + mh;
+  const int nb = J.nb, ib = J.ib, ntile = L.ntile, wsz = J.wsz;
+  const int nblk = J.b_hi - J.b_lo;
+  const bool active = 16 * mh < wsz;                  // a column group beyond a narrow strip idles
+  auto blk = [&](int idx) { return J.trans ? J.b_lo + idx : J.b_hi - 1 - idx; };
 
   for (int idx = 0; idx < nblk; ++idx) {
-    const int cur = idx & 1;
+    const int cur = (base + idx) & 1;
     const int b = blk(idx);
     const int j0 = b * ib, bw = min(ib, nb - j0);
     int blo, bhi;
@@ -865,28 +885,87 @@ __device__ void strip_update(const StripJob &J, double *smem, const SmemLayout &
       if (last) s_done[cur] = 0;
       __threadfence_block();
     }
-    if (__shfl_sync(0xffffffffu, last, 0) && idx + 2 < nblk) su_issue<KIND>(J, L, smem, cur, blk(idx + 2));
-  }
-
-  // ---- C strip back to global (only the rows and columns this task owns)
-#pragma unroll
-  for (int s = 0; s < kSlots; ++s) {
-    const int j = su_tile<KIND>(rg, s, ntile), r = 8 * j + 2 * t;
-    const bool act = s < ntask && r < nb;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int col = cg + 8 * h;
-      if (act && col < wsz) {
-        double *dst = J.C2 + r + (size_t)(J.cs + col) * nb;
-        if (even) {
-          *reinterpret_cast<double2 *>(dst) = make_double2(acc[s][2 * h], acc[s][2 * h + 1]);
-        } else {
-          dst[0] = acc[s][2 * h];
-          if (r + 1 < nb) dst[1] = acc[s][2 * h + 1];
-        }
+    if (__shfl_sync(0xffffffffu, last, 0)) {
+      if (idx + 2 < nblk) {
+        su_issue<KIND>(J, L, smem, cur, blk(idx + 2));
+      } else if (KIND == SU_UN && JN != nullptr) {
+        const int n = idx + 2 - nblk;
+        if (n < JN->b_hi - JN->b_lo) su_issue<SU_TT>(*JN, L, smem, cur, JN->trans ? JN->b_lo + n : JN->b_hi - 1 - n);
       }
     }
   }
+}
+
+template <int KIND>
+__device__ void strip_update(const StripJob &J, double *smem, const SmemLayout &L, unsigned &ph) {
+  const int warp = threadIdx.x >> 5;
+  // two independent column groups (warps 0-3: columns 0-15, warps 4-7:
+  // columns 16-31), one warp per SM sub-partition each, synchronised only by
+  // their own named barriers: one group's latency-bound steps (reduction,
+  // phase 2, copy issue) overlap the other group's DMMA phases
+  // the row groups of column group 1 are rotated by one against group 0's, so
+  // the row group with an extra row tile (n_tiles % 4 != 0) lands on two
+  // different sub-partitions (warp w runs on sub-partition w % 4)
+  const int mh = warp >> 2, rg = (warp + mh) & 3;
+  const int ib = J.ib, nb = J.nb, ntile = L.ntile;
+  const int nblk = J.b_hi - J.b_lo;
+  int ct_lo = 0, ct_hi = ntile;                       // row tiles of C this task touches
+  if (KIND == SU_UN) ct_lo = (J.b_lo * ib) >> 3;
+  if (KIND == SU_TT) ct_hi = (min(J.b_hi * ib, nb) + 7) >> 3;
+  const int ntask = su_nact<KIND>(rg, ct_lo, ct_hi, ntile);   // slots holding C rows of this task
+  const bool wait0 = !J.resident || KIND != SU_UN;     // resident TT/TS blocks still load their C1 window
+  auto blk = [&](int idx) { return J.trans ? J.b_lo + idx : J.b_hi - 1 - idx; };
+  if (warp == 0) {                                    // both buffers are free: blocks 0 and 1
+    if (wait0) su_issue<KIND>(J, L, smem, 0, blk(0), !J.resident);
+    if (nblk > 1) su_issue<KIND>(J, L, smem, 1, blk(1));
+  }
+  double acc[kSlots][4];
+  su_load_c<KIND>(J, acc, rg, ntask, ntile);
+  su_loop<KIND>(J, nullptr, smem, L, ph, acc, rg, 0, wait0);
+  su_store_c<KIND>(J, acc, rg, ntask, ntile);
+}
+
+// Fused UNMQR + TTMQR of one strip of tile (i, j) (K_UNTTMQR): the UNMQR by
+// GEQRT(i, k)'s reflectors (JU) and then the TTMQR by TTQRT(i, piv, k)'s (JT)
+// with the strip of tile (i, j) kept in registers between the two, and the
+// TT job's first blocks streamed in behind the UN job's last ones. Both jobs
+// cover all blocks, so every row tile is live. The UN loop deals row tiles
+// bottom-up (tile ntile-1-rg-4s), the TT loop top-down (tile rg'+4s'): with
+// rg' = (ntile-1-rg) & 3 a warp keeps the same row tiles, in reversed slot
+// order, so the hand-over is a register permutation. Same arithmetic, in the
+// same order, as the two separate tasks (bit-identical results).
+__device__ void strip_update_untt(const StripJob &JU, const StripJob &JT, double *smem, const SmemLayout &L,
+                                  unsigned &ph) {
+  const int warp = threadIdx.x >> 5;
+  const int mh = warp >> 2, rg = (warp + mh) & 3;
+  const int ntile = L.ntile;
+  const int rg2 = (ntile - 1 - rg) & 3;
+  const int nu = JU.b_hi - JU.b_lo, nt = JT.b_hi - JT.b_lo;
+  const int ntask = su_nact<SU_UN>(rg, 0, ntile, ntile);
+  if (warp == 0) {   // sequence blocks 0 and 1 (UN blocks, then TT blocks)
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      if (x < nu) su_issue<SU_UN>(JU, L, smem, x, JU.trans ? JU.b_lo + x : JU.b_hi - 1 - x);
+      else if (x - nu < nt) su_issue<SU_TT>(JT, L, smem, x, JT.trans ? JT.b_lo + x - nu : JT.b_hi - 1 - (x - nu));
+    }
+  }
+  double acc[kSlots][4];
+  su_load_c<SU_UN>(JU, acc, rg, ntask, ntile);
+  su_loop<SU_UN>(JU, &JT, smem, L, ph, acc, rg, 0, true);
+  // slot s (tile ntile-1-rg-4s) -> slot ntask-1-s (tile rg2 + 4(ntask-1-s))
+#define TQR_REV(M)                                                  \
+  {                                                                 \
+    double tmp[kSlots][4];                                          \
+    _Pragma("unroll") for (int s = 0; s < kSlots; ++s)              \
+    _Pragma("unroll") for (int e = 0; e < 4; ++e)                   \
+      tmp[s][e] = s < (M) ? acc[(M) - 1 - s][e] : 0.0;              \
+    _Pragma("unroll") for (int s = 0; s < kSlots; ++s)              \
+    _Pragma("unroll") for (int e = 0; e < 4; ++e) acc[s][e] = tmp[s][e]; \
+  }
+  TQR_SLOT_SWITCH(ntask, TQR_REV)
+#undef TQR_REV
+  su_loop<SU_TT>(JT, nullptr, smem, L, ph, acc, rg2, nu & 1, true);
+  su_store_c<SU_TT>(JT, acc, rg2, ntask, ntile);
 }
 
 // ---- panel kernels: GEQRT / TTQRT / TSQRT on whole tiles ------------------
@@ -974,6 +1053,20 @@ __device__ void run_task(const RunArgs &a, const DevTask &t, double *smem, const
                          tile_ptr(Cbase, p, nb, t.i, t.j), nb, ib, cs, min(ws, nb - cs), 0, nblk, a.trans != 0, false,
                          mA, t.kind == K_UNMQR ? mA : mC, col(t.i, t.k), 0};
         strip_update<SU_UN>(J, smem, L, ph);
+      }
+      break;
+    }
+    case K_UNTTMQR: {   // fused UNMQR by GEQRT(i, k) + TTMQR by TTQRT(i, piv, k) of tile (i, j)
+      for (int u = 0; u < max(t.pad, 1); ++u) {
+        if (u > 0) __syncthreads();
+        const int cs = (t.s + u) * ws;
+        double *Ci = tile_ptr(a.A, p, nb, t.i, t.j);
+        const StripJob JU{tile_ptr(a.A, p, nb, t.i, t.k), tslot_ptr(a.T, p, nb, ib, t.i, t.k, 0), nullptr, Ci, nb, ib,
+                          cs, min(ws, nb - cs), 0, nblk, true, false, mA, mA, col(t.i, t.k), 0};
+        const StripJob JT{tile_ptr(a.A, p, nb, t.i, t.k), tslot_ptr(a.T, p, nb, ib, t.i, t.k, 1),
+                          tile_ptr(a.A, p, nb, t.piv, t.j), Ci, nb, ib, cs, min(ws, nb - cs), 0, nblk, true, false,
+                          mA, mA, col(t.i, t.k), col(t.piv, t.j)};
+        strip_update_untt(JU, JT, smem, L, ph);
       }
       break;
     }

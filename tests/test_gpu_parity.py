@@ -385,7 +385,8 @@ def test_host_async_pipeline():
 
 
 SCHED_MODES = [{}, {"TQR_WORK_FIRST": "0"}, {"TQR_CHAIN_SPIN": "64"}, {"TQR_PRIO": "1"}, {"TQR_PRIO": "3"},
-               {"TQR_LEVELS": "2"}, {"TQR_LOOKAHEAD": "0"}, {"TQR_GRID": "5"}, {"TQR_GRID": "1"}, {"TQR_TMA": "1"}]
+               {"TQR_LEVELS": "2"}, {"TQR_LOOKAHEAD": "0"}, {"TQR_GRID": "5"}, {"TQR_GRID": "1"}, {"TQR_TMA": "1"},
+               {"TQR_FUSE": "1"}]
 
 
 @pytest.mark.parametrize("tree,bs,family", [("greedy", 1, "TT"), ("plasma", 3, "TS"), ("asap", 1, "TT")])
@@ -399,7 +400,8 @@ def test_schedule_invariance(tree, bs, family, monkeypatch):
     A = qrinputs.gaussian(m, n, 77)
     ref = None
     for mode in SCHED_MODES:
-        for k in ("TQR_WORK_FIRST", "TQR_CHAIN_SPIN", "TQR_PRIO", "TQR_LEVELS", "TQR_LOOKAHEAD", "TQR_GRID", "TQR_TMA"):
+        for k in ("TQR_WORK_FIRST", "TQR_CHAIN_SPIN", "TQR_PRIO", "TQR_LEVELS", "TQR_LOOKAHEAD", "TQR_GRID", "TQR_TMA",
+                  "TQR_FUSE"):
             monkeypatch.delenv(k, raising=False)
         for k, v in mode.items():
             monkeypatch.setenv(k, v)
@@ -412,6 +414,29 @@ def test_schedule_invariance(tree, bs, family, monkeypatch):
             assert rel(nu.sign_normalise(R), nu.sign_normalise(np.linalg.qr(A, mode="r"))) <= TOL_R
         else:
             assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1]), mode
+
+
+@pytest.mark.parametrize("p,q,nb,tree,tma", [(6, 4, 200, "flat", "1"), (5, 4, 200, "greedy", "1"),
+                                             (6, 3, 256, "fibonacci", "1"), (8, 4, 32, "flat", "1"),
+                                             (7, 3, 72, "greedy", "0"), (6, 3, 50, "flat", "1"),
+                                             (5, 3, 200, "flat", "0")])
+def test_fused_unttmqr_bitwise(p, q, nb, tree, tma, monkeypatch):
+    """UNMQR + TTMQR fusion (K_UNTTMQR, TQR_FUSE=1; off by default) runs the same
+    arithmetic in the same order as the two separate tasks: A (R and V) and T
+    are bitwise identical with and without it, on both copy paths, at nb with
+    one inner block (32), a ragged last inner block (nb = 200, 72, 50) and nb = 256;
+    and the fused result equals the oracle."""
+    ib = 32
+    A = qrinputs.gaussian(p * nb, q * nb, 900 + p + nb)
+    monkeypatch.setenv("TQR_TMA", tma)
+    monkeypatch.setenv("TQR_FUSE", "0")
+    b0, T0 = run_gpu(A, nb, ib, tree, 1, "TT")
+    monkeypatch.setenv("TQR_FUSE", "1")
+    b1, T1 = run_gpu(A, nb, ib, tree, 1, "TT")
+    assert torch.equal(b0, b1) and torch.equal(T0, T1)
+    F = nu.tiled_qr(A, nb, ib, schemes.elim_list(tree, p, q), "TT")
+    got = qrinputs.from_tiles(b1.cpu().numpy(), p, q, nb)
+    assert rel(got, F.A) <= TOL_R and np.abs(got - F.A).max() <= TOL_R * np.abs(F.A).max()
 
 
 def test_strip_width_too_wide_is_rejected(monkeypatch):

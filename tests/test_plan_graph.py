@@ -46,7 +46,7 @@ def writes(t, nb, ib, ws):
         return {((i, k), s), ((piv, k), s)}
     if name == "UNMQR":
         return {((i, j), s + u) for u in range(ns)}
-    if name in ("TTMQR", "TSMQR"):
+    if name in ("TTMQR", "TSMQR", "UNTTMQR"):
         return {((i, j), s + u) for u in range(ns)} | {((piv, j), s + u) for u in range(ns)}
     if name == "GEQRT":
         return {((i, k), x) for x in range(-(-nb // ws))}
@@ -59,12 +59,36 @@ CASES = [("greedy", 1, "TT"), ("flat", 1, "TS"), ("fibonacci", 1, "TT"), ("binar
          ("plasma", 3, "TS")]
 
 
+def fused_pairs(tiles):
+    """UNMQR(i,k,j) whose next task on tile (i,j), in emission order, is the
+    TTMQR(i,piv,k,j) eliminating the same row: these run as one UNTTMQR task."""
+    last, pairs = {}, 0
+    for t in tiles:
+        if t.kind == "GEQRT":
+            touched = [(t.i, t.k)]
+        elif t.kind == "UNMQR":
+            touched = [(t.i, t.j)]
+        elif t.kind in ("TTQRT", "TSQRT"):
+            touched = [(t.i, t.k), (t.piv, t.k)]
+        else:
+            touched = [(t.i, t.j), (t.piv, t.j)]
+        for tile in touched:
+            u = last.get(tile)
+            if (u is not None and tile == (t.i, t.j) and u.kind == "UNMQR" and t.kind == "TTMQR"
+                    and (u.i, u.k, u.j) == (t.i, t.k, t.j)):
+                pairs += 1
+            last[tile] = t
+    return pairs
+
+
 @pytest.mark.parametrize("tree,bs,family", CASES)
-@pytest.mark.parametrize("p,q,nb,split,mstrip", [(6, 3, 72, True, 1), (6, 3, 72, True, 2), (5, 2, 64, True, 2),
-                                                  (4, 4, 64, False, 1), (4, 3, 200, True, 3)])
-def test_plan_graph_invariants(tree, bs, family, p, q, nb, split, mstrip):
+@pytest.mark.parametrize("p,q,nb,split,mstrip,fuse", [(6, 3, 72, True, 1, False), (6, 3, 72, True, 1, True),
+                                                       (6, 3, 72, True, 2, True), (5, 2, 64, True, 2, True),
+                                                       (4, 4, 64, False, 1, True), (4, 3, 200, True, 3, True),
+                                                       (4, 3, 200, True, 3, False)])
+def test_plan_graph_invariants(tree, bs, family, p, q, nb, split, mstrip, fuse):
     ib = ws = 32
-    tasks, ptr, succ = tq.plan_graph(p * nb, q * nb, nb, ib, tree, bs, family, ws, split, mstrip)
+    tasks, ptr, succ = tq.plan_graph(p * nb, q * nb, nb, ib, tree, bs, family, ws, split, mstrip, fuse)
     n = len(tasks)
     # topological priority order and indegrees
     indeg = np.zeros(n, np.int64)
@@ -102,10 +126,13 @@ def test_plan_graph_invariants(tree, bs, family, p, q, nb, split, mstrip):
         i, k = int(tasks[t, 1]), int(tasks[t, 3])
         src = ("ge", i, k) if name in ("UNMQR", "GEQRT_U") else (("tp", i, k) if name in (
             "TTMQR", "TSMQR", "TTQRT_U", "TSQRT_U") else None)
-        if src is None:
+        if name == "UNTTMQR":   # reads GEQRT(i,k)'s and TTQRT(i,piv,k)'s reflectors
+            need = panel_of[("ge", i, k)] + panel_of[("tp", i, k)]
+        elif src is None:
             continue
-        need = panel_of[src] if name in ("UNMQR", "TTMQR", "TSMQR") else [
-            u for u in panel_of[src] if int(tasks[u, 5]) & 0xFFFF == int(tasks[t, 4])]
+        else:
+            need = panel_of[src] if name in ("UNMQR", "TTMQR", "TSMQR") else [
+                u for u in panel_of[src] if int(tasks[u, 5]) & 0xFFFF == int(tasks[t, 4])]
         for u in need:
             assert (r[u] >> t) & 1, (name, src)
     # task counts from the tile-level DAG
@@ -120,6 +147,14 @@ def test_plan_graph_invariants(tree, bs, family, p, q, nb, split, mstrip):
             expect += nblk + nblk * (nblk - 1) // 2
         else:
             expect += 1
+    if fuse:
+        npair = fused_pairs(tiles)
+        expect -= npair * -(-S // mstrip)
+        assert (tasks[:, 0] == tq.KIND_NAMES.index("UNTTMQR")).sum() == npair * -(-S // mstrip)
+        if family == "TT" and q > 1:
+            assert npair > 0
+    else:
+        assert not (tasks[:, 0] == tq.KIND_NAMES.index("UNTTMQR")).any()
     assert n == expect
 
 
