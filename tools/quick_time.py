@@ -16,17 +16,18 @@ A = torch.empty_like(A0)
 T = torch.empty(tq.t_size(m, n, nb, ib), dtype=torch.float64, device="cuda")
 flops = 2.0 * n * n * (m - n / 3.0)
 for spec in trees:
-    tree, bs = (spec.split(":") + ["1"])[:2]
+    parts = spec.split(":")
+    tree, bs, fam = parts[0], parts[1] if len(parts) > 1 else "1", parts[2] if len(parts) > 2 else "TT"
     bs = int(bs)
     ts = []
     for it in range(5):
         A.copy_(A0)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        tq.tiled_qr(A, m, n, nb, ib, tree, bs, "TT", T=T)
+        tq.tiled_qr(A, m, n, nb, ib, tree, bs, fam, T=T)
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     best = min(ts[1:])
-    print(f"{tree}:{bs} p={p} q={q} nb={nb}: {best:.3f} ms  {flops / best / 1e9:.1f} TFLOP/s  (all {['%.2f' % t for t in ts]})",
+    print(f"{tree}:{bs}:{fam} p={p} q={q} nb={nb}: {best:.3f} ms  {flops / best / 1e9:.1f} TFLOP/s  (all {['%.2f' % t for t in ts]})",
           flush=True)
