@@ -6,7 +6,8 @@ nb = 200 (8000 x 8000 fp64, i.i.d. N(0,1), ib = 32; §4 lines
 configs[2] names — Greedy, Fibonacci, FlatTree (Sameh-Kuck) — and each kernel
 family (TT and TS, Algorithms 3 and 2): 6 factorizations.
 value = 2n^2(m-n/3) flops x 6 / device time (GFLOP/s). The same line carries
-configs[3] on one GPU (`tall_1gpu`: 524288 x 4096, nb = 256, Greedy TT).
+configs[3] on one GPU (`tall_1gpu`: 524288 x 4096, nb = 256, Greedy with TS kernels, `--family`;
+it also lists the same factorization by tree and kernel family).
 
 N > 1 (`--gpus N`; relaunches itself under torch.distributed.run when
 WORLD_SIZE is unset): configs[3] partitioned — contiguous tile-row domains per
@@ -359,7 +360,7 @@ def run_tall(args, rank, world, local_rank, nested=False):
 
     p = args.tall_p or TALL["p"]
     q, nb = TALL["q"], TALL["nb"]
-    tree = args.tree
+    tree, fam = args.tree, args.family
     m, n = p * nb, q * nb
     flops = flops_qr(m, n)
     torch.cuda.set_device(local_rank)
@@ -379,7 +380,7 @@ def run_tall(args, rank, world, local_rank, nested=False):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        tdist.tall_skinny_qr(A, p, q, nb, IB, tree, 1, "TT")
+        tdist.tall_skinny_qr(A, p, q, nb, IB, tree, 1, fam)
         e1.record(stream)
         times.append((e0, e1))
 
@@ -416,7 +417,7 @@ def run_tall(args, rank, world, local_rank, nested=False):
 
         def e2e_step():
             A.copy_(pin, non_blocking=True)
-            F = tdist.tall_skinny_qr(A, p, q, nb, IB, tree, 1, "TT")
+            F = tdist.tall_skinny_qr(A, p, q, nb, IB, tree, 1, fam)
             if F.R is not None:
                 r_host.copy_(F.R, non_blocking=True)
 
@@ -445,8 +446,10 @@ def run_tall(args, rank, world, local_rank, nested=False):
         "warmup": warm, "ms_per_step": max_ms / steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"configs[3]: tall-skinny fp64 tiled QR {m}x{n} (p={p} x q={q} tiles, nb={nb}, "
-                               f"ib={IB}), i.i.d. N(0,1), tile-row domains per GPU reduced locally by {tree}, "
-                               f"then a binary TT merge of the q x q R factors across GPUs (NCCL send/recv)",
+                               f"ib={IB}), i.i.d. N(0,1), tile-row domains per GPU reduced locally by {tree} "
+                               f"with {fam} kernels, then a binary TT merge of the q x q R factors across GPUs "
+                               f"(NCCL send/recv)",
+                   "tree": tree, "family": fam,
                    "parallelism": f"tile-row domains x{world}",
                    "l2": "inputs (17 GB at full size) far exceed L2; restored by a device copy outside the events",
                    "timing": "CUDA events around tall_skinny_qr per rank (local factor + merges + NCCL), max over ranks"},
@@ -458,6 +461,25 @@ def run_tall(args, rank, world, local_rank, nested=False):
         "e2e": e2e,
         "gpu_launches": (1 + merges) * steps,
     }
+    if nested and world == 1 and not args.tall_p:
+        # the same 1-GPU factorization by tree and kernel family (one warm-up, one timed run each):
+        # TS kernels on full tiles keep the tensor pipe busier
+        by = {}
+        T = torch.empty(tq.t_size(m, n, nb, IB), dtype=torch.float64, device=dev)
+        for tr, bs, fm in (("greedy", 1, "TT"), ("greedy", 1, "TS"), ("flat", 1, "TS"), ("plasma", 64, "TS")):
+            ts = []
+            for _ in range(2):
+                A.copy_(A0)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                tq.tiled_qr(A, m, n, nb, IB, tr, bs, fm, T=T)
+                e1.record(stream)
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            by[f"{tr}:{bs} {fm}"] = flops / (ts[-1] / 1e3) / 1e9
+        out["local_by_tree_gflops"] = by
+        del T
     del A0, A
     torch.cuda.empty_cache()
     if nested:
@@ -540,6 +562,8 @@ def main():
                     help="auto = configs[2] at N=1, configs[3] partitioned at N>1; cfg1 = configs[1]; "
                          "qsweep = configs[4] table (1 GPU)")
     ap.add_argument("--tree", default="greedy", help="tree of the local factorizations (tall workload)")
+    ap.add_argument("--family", default="TS", choices=["TT", "TS"],
+                    help="kernel family of the local factorizations (tall workload; the merge is TT)")
     ap.add_argument("--tall-p", type=int, default=0, help="override p of the tall workload (testing)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

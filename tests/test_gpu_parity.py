@@ -277,8 +277,9 @@ def test_merge_kernel(q, nb, ib, family):
     assert np.linalg.norm(np.eye(n) - Q.T @ Q) <= TOL_QR
 
 
-@pytest.mark.parametrize("world,tree", [(4, "greedy"), (3, "fibonacci"), (2, "flat")])
-def test_tall_skinny_domains_on_one_gpu(world, tree):
+@pytest.mark.parametrize("world,tree,family", [(4, "greedy", "TT"), (3, "fibonacci", "TT"), (2, "flat", "TT"),
+                                               (4, "greedy", "TS"), (2, "plasma", "TS")])
+def test_tall_skinny_domains_on_one_gpu(world, tree, family):
     """The configs[3] algorithm with `world` domains executed one after another on
     one GPU (independent launches, no inter-kernel waiting): local tiled QR per
     domain, then the binary merge tree of paper_1104_4475_b200.dist; the final R
@@ -290,7 +291,7 @@ def test_tall_skinny_domains_on_one_gpu(world, tree):
     for r in range(world):
         r0, r1 = tdist.domain(p, world, r)
         loc = torch.from_numpy(qrinputs.to_tiles(np.asfortranarray(A[r0 * nb:r1 * nb]), nb)).to(DEV)
-        tq.tiled_qr(loc, (r1 - r0) * nb, q * nb, nb, ib, tree, 1, "TT")
+        tq.tiled_qr(loc, (r1 - r0) * nb, q * nb, nb, ib, tree, 2 if tree == "plasma" else 1, family)
         Rs.append(tdist.extract_r(loc, r1 - r0, q, nb))
     for pairs in tdist.merge_schedule(world):
         for dst, src in pairs:
@@ -344,9 +345,10 @@ def test_config2_square_full_size(tree, family):
 _LAPACK_R = {}
 
 
-def test_config3_tall_full_size_gram():
+@pytest.mark.parametrize("family", ["TT", "TS"])
+def test_config3_tall_full_size_gram(family):
     """configs[3] as `bench.py --workload tall` runs it on one GPU: 524288 x 4096
-    (p = 2048, q = 16, nb = 256), Greedy. The oracle cannot run at this size, so
+    (p = 2048, q = 16, nb = 256), Greedy, TT and TS kernels. The oracle cannot run at this size, so
     check properties that hold at any size: R^T R = A^T A (A = QR with Q
     orthonormal), and R equals the Cholesky factor of A^T A up to row signs."""
     p, q, nb, ib = 2048, 16, 256, 32
@@ -356,7 +358,7 @@ def test_config3_tall_full_size_gram():
     Ad = tq.from_tiled(A, m, n, nb)
     G = Ad.T @ Ad
     del Ad
-    tq.tiled_qr(A, m, n, nb, ib, "greedy")
+    tq.tiled_qr(A, m, n, nb, ib, "greedy", 1, family)
     R = torch.triu(tq.from_tiled(A, m, n, nb)[:n])
     err = (torch.linalg.norm(R.T @ R - G) / torch.linalg.norm(G)).item()
     assert err <= 1e-13, err
@@ -518,8 +520,9 @@ class _Mailbox:
         return _End()
 
 
-@pytest.mark.parametrize("world,tree", [(2, "greedy"), (3, "fibonacci"), (4, "flat")])
-def test_distributed_apply_threads(world, tree):
+@pytest.mark.parametrize("world,tree,family", [(2, "greedy", "TT"), (3, "fibonacci", "TT"), (4, "flat", "TT"),
+                                               (2, "greedy", "TS"), (3, "flat", "TS")])
+def test_distributed_apply_threads(world, tree, family):
     """dist.tall_skinny_qr + dist.apply_qt / apply_q with the CUDA kernels, the ranks
     run as threads on one GPU (mailbox exchange): Q^T [A | X] gives R on top and
     zeros below it for the A columns, least squares matches numpy, Q undoes Q^T."""
@@ -538,7 +541,7 @@ def test_distributed_apply_threads(world, tree):
             A_loc = torch.from_numpy(qrinputs.to_tiles(np.asfortranarray(A[r0 * nb:r1 * nb]), nb)).to(DEV)
             B_loc = torch.from_numpy(qrinputs.to_tiles(np.asfortranarray(B[r0 * nb:r1 * nb]), nb)).to(DEV)
             comm = box.endpoint(rank)
-            F = tdist.tall_skinny_qr(A_loc, p, q, nb, ib, tree, 1, "TT", comm=comm)
+            F = tdist.tall_skinny_qr(A_loc, p, q, nb, ib, tree, 1, family, comm=comm)
             tdist.apply_qt(F, B_loc, qc * nb, comm=comm)
             torch.cuda.synchronize()
             out[f"qtb{rank}"] = qrinputs.from_tiles(B_loc.cpu().numpy(), r1 - r0, qc, nb)
