@@ -197,7 +197,7 @@ def run_reference(args, rank, world):
     v = float(np.mean(vals))
     g, fl, nt, tot, thr, el = last
     sample = (f"first {nt} of {tot} tasks (in list order) of the Greedy TT factorization of a {p}x{q}-tile "
-              f"nb={nb} matrix, {budget:.0f} s budget per step, oracle/numeric.py kernels (numpy fp64)")
+              f"nb={nb} matrix, {budget:g} s budget per step, oracle/numeric.py kernels (numpy fp64)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": budget * 1000.0, "higher_is_better": True,
