@@ -21,6 +21,7 @@ constexpr int kMaxNb = 256;
 constexpr int kMaxIb = 32;
 constexpr size_t kMaxSmem = 227 * 1024 - 512;   // dynamic smem budget (opt-in max minus static)
 constexpr int kTld = 33;
+constexpr int kLdwP = 34;                   // partial W^T: accumulator-pattern stores and loads only (col + 2t*kLdwP conflict-free)
 constexpr int kLdw = 36;                    // W^T / W2^T in smem: element (col, refl) at col + refl * kLdw
 constexpr int kSlots = 8;                   // row tiles of 8 per warp in a strip update (nb <= 256)
 #ifndef TQR_BOX
@@ -367,6 +368,9 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+#ifndef TQR_PABL
+#define TQR_PABL 0   // tools/panel_bench.cu only: timing attribution of the column chain (results are wrong)
+#endif
 template <int MODE>
 __device__ void panel_block(double *X, double *A1, double *Tslot, int nb, int ib, int j0, int bw,
                             double *Vbuf, double *Tb, double *scratch) {
@@ -414,10 +418,11 @@ __device__ void panel_block(double *X, double *A1, double *Tslot, int nb, int ib
           const int rr = lane + 32 * s2;
           if (rr >= first && rr <= last) ss = fma(a[qo][s2], a[qo][s2], ss);
         }
-        const double xn2 = warp_sum(ss);
+        const double xn2 = (TQR_PABL & 2) ? ss : warp_sum(ss);
         const double alpha = __shfl_sync(0xffffffffu, MODE == 0 ? a[qo][0] : pt[qo], c);
         double beta, tau, scale;
-        larfg_scalars(alpha, xn2, beta, tau, scale);
+        if (TQR_PABL & 1) { beta = alpha; tau = 0.5; scale = 1e-3 * xn2; }
+        else larfg_scalars(alpha, xn2, beta, tau, scale);
 #pragma unroll
         for (int s2 = 0; s2 < 8; ++s2) {
           const int rr = lane + 32 * s2;
@@ -429,7 +434,7 @@ __device__ void panel_block(double *X, double *A1, double *Tslot, int nb, int ib
         if (lane == c) betas[qo] = beta;
         if (lane == 0) { scal[(c & 1) * 4] = tau; taus[c] = tau; }
       }
-      __syncthreads();
+      if (!(TQR_PABL & 8)) __syncthreads();
       // ---- apply reflector c to the owned columns > c ----
       // branch-free over the 4 owned columns so the 4 warp reductions overlap
       const double tau = scal[(c & 1) * 4];
@@ -445,10 +450,11 @@ __device__ void panel_block(double *X, double *A1, double *Tslot, int nb, int ib
 #pragma unroll
             for (int s2 = 0; s2 < 8; ++s2) d[q] = fma(v[s2], a[q][s2], d[q]);
           }
-          P[q] = MODE == 0 ? __shfl_sync(0xffffffffu, a[q][0], c) : __shfl_sync(0xffffffffu, pt[q], c);
+          P[q] = (TQR_PABL & 16) ? a[q][1]
+                 : MODE == 0 ? __shfl_sync(0xffffffffu, a[q][0], c) : __shfl_sync(0xffffffffu, pt[q], c);
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
+        for (int o = (TQR_PABL & 4) ? 0 : 16; o > 0; o >>= 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             if (q >= qo) d[q] += __shfl_xor_sync(0xffffffffu, d[q], o);
@@ -798,37 +804,51 @@ __device__ __forceinline__ void su_loop(const StripJob &J, const StripJob *JN, d
     }
 #undef TQR_P1
     {
-      double *Wp = smem + L.offWp + rg * 32 * kLdw;
+      double *Wp = smem + L.offWp + rg * 32 * kLdwP;
 #pragma unroll
       for (int nn = 0; nn < 4; ++nn) {
         const int rf = 8 * nn + 2 * t;
-        Wp[cg + rf * kLdw] = wacc[nn][0];
-        Wp[cg + (rf + 1) * kLdw] = wacc[nn][1];
-        Wp[cg + 8 + rf * kLdw] = wacc[nn][2];
-        Wp[cg + 8 + (rf + 1) * kLdw] = wacc[nn][3];
+        Wp[cg + rf * kLdwP] = wacc[nn][0];
+        Wp[cg + (rf + 1) * kLdwP] = wacc[nn][1];
+        Wp[cg + 8 + rf * kLdwP] = wacc[nn][2];
+        Wp[cg + 8 + (rf + 1) * kLdwP] = wacc[nn][3];
       }
     }
     group_sync(gbar);
     prof_mark(PH_MMA1);
 
-    // ---- phase 2: W2^T fragment (columns 16 mh.., reflectors 8 rg..) = -W^T op(T)^T,
-    // W^T = the group's 4 partials (+ the C1 window: identity part of V), summed
-    // while loading the A fragments
+    // ---- reduction: W^T = the group's 4 partials (+ the C1 window: identity part of V);
+    // every warp reduces the accumulator positions of its own n-tile rg (a quarter of
+    // the group's W^T) instead of all four warps summing all of it while loading
+    double2 c1w[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
     {
       const double *Wp0 = smem + L.offWp;
+      double *W = smem + L.offW;
+      const int rf = 8 * rg + 2 * t;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int o = cg + 8 * h + rf * kLdwP, ow = cg + 8 * h + rf * kLdw;
+        double r0 = (Wp0[o] + Wp0[o + 32 * kLdwP]) + (Wp0[o + 64 * kLdwP] + Wp0[o + 96 * kLdwP]);
+        double r1 = (Wp0[o + kLdwP] + Wp0[o + kLdwP + 32 * kLdwP]) + (Wp0[o + kLdwP + 64 * kLdwP] + Wp0[o + kLdwP + 96 * kLdwP]);
+        if (KIND != SU_UN) {
+          c1w[h] = *reinterpret_cast<const double2 *>(C1w + rg * 256 + (cg + 8 * h) * 8 + 2 * t);
+          r0 += c1w[h].x;
+          r1 += c1w[h].y;
+        }
+        W[ow] = r0;
+        W[ow + kLdw] = r1;
+      }
+    }
+    group_sync(gbar);
+    // ---- phase 2: W2^T fragment (columns 16 mh.., reflectors 8 rg..) = -W^T op(T)^T
+    {
+      const double *Wr = smem + L.offW;
       double *W2 = smem + L.offW2;
       double a2[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
-        const int o0 = (16 * mh + g) + (4 * kk + t) * kLdw, o1 = o0 + 8;
-        double a0 = (Wp0[o0] + Wp0[o0 + 32 * kLdw]) + (Wp0[o0 + 64 * kLdw] + Wp0[o0 + 96 * kLdw]);
-        double a1 = (Wp0[o1] + Wp0[o1 + 32 * kLdw]) + (Wp0[o1 + 64 * kLdw] + Wp0[o1 + 96 * kLdw]);
-        if (KIND != SU_UN) {   // C1_b[refl 4kk+t][col]: row-tile layout of the window
-          const int rf = 4 * kk + t;
-          a0 += C1w[(rf >> 3) * 256 + (16 * mh + g) * 8 + (rf & 7)];
-          a1 += C1w[(rf >> 3) * 256 + (16 * mh + g + 8) * 8 + (rf & 7)];
-        }
-        dmma(a2[kk & 1], a0, a1, tb[kk]);
+        const int o0 = (16 * mh + g) + (4 * kk + t) * kLdw;
+        dmma(a2[kk & 1], Wr[o0], Wr[o0 + 8], tb[kk]);
       }
       prof_mark(PH_FIX);
       double w2[4];
@@ -844,7 +864,7 @@ __device__ __forceinline__ void su_loop(const StripJob &J, const StripJob *JN, d
         for (int h = 0; h < 2; ++h) {
           const int col = 16 * mh + g + 8 * h;
           if (col < wsz && rf < bw) {
-            const double2 c1 = *reinterpret_cast<const double2 *>(C1w + rg * 256 + col * 8 + 2 * t);
+            const double2 c1 = c1w[h];
             double *dst = J.C1 + (j0 + rf) + (size_t)(J.cs + col) * nb;
             const double v0 = c1.x + w2[2 * h], v1 = c1.y + w2[2 * h + 1];
             if (rf + 1 < bw && ((nb | j0) & 1) == 0) {
