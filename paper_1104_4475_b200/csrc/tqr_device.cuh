@@ -784,13 +784,6 @@ __device__ __forceinline__ void su_loop(const StripJob &J, const StripJob *JN, d
     prof_mark(idx == 0 ? PH_LOAD : PH_PANEL);   // (tracer: first copy wait vs later ones)
     double *Vb = smem + L.offV[cur];
     const double *Tb = smem + L.offT[cur], *C1w = smem + L.offC1[cur];
-    // phase-2 B operand: op(T)^T fragments of this warp's n-tile (T upper triangular, zero-padded)
-    double tb[8];
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const int r = J.trans ? 4 * kk + t : 8 * rg + g, c = J.trans ? 8 * rg + g : 4 * kk + t;
-      tb[kk] = (r <= c && c < bw) ? Tb[r + c * ib] : 0.0;
-    }
 
     // ---- phase 1: partial W^T (16 columns x 32 reflectors) over this warp's row tiles
     double wacc[4][4];
@@ -817,6 +810,13 @@ __device__ __forceinline__ void su_loop(const StripJob &J, const StripJob *JN, d
     group_sync(gbar);
     prof_mark(PH_MMA1);
 
+    // phase-2 B operand (loaded here, not at block start: 16 registers less across phase 1): op(T)^T fragments of this warp's n-tile (T upper triangular, zero-padded)
+    double tb[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int r = J.trans ? 4 * kk + t : 8 * rg + g, c = J.trans ? 8 * rg + g : 4 * kk + t;
+      tb[kk] = (r <= c && c < bw) ? Tb[r + c * ib] : 0.0;
+    }
     // ---- reduction: W^T = the group's 4 partials (+ the C1 window: identity part of V);
     // every warp reduces the accumulator positions of its own n-tile rg (a quarter of
     // the group's W^T) instead of all four warps summing all of it while loading
