@@ -807,9 +807,6 @@ __device__ __forceinline__ void su_loop(const StripJob &J, const StripJob *JN, d
         Wp[cg + 8 + (rf + 1) * kLdwP] = wacc[nn][3];
       }
     }
-    group_sync(gbar);
-    prof_mark(PH_MMA1);
-
     // phase-2 B operand (loaded here, not at block start: 16 registers less across phase 1): op(T)^T fragments of this warp's n-tile (T upper triangular, zero-padded)
     double tb[8];
 #pragma unroll
@@ -817,6 +814,9 @@ __device__ __forceinline__ void su_loop(const StripJob &J, const StripJob *JN, d
       const int r = J.trans ? 4 * kk + t : 8 * rg + g, c = J.trans ? 8 * rg + g : 4 * kk + t;
       tb[kk] = (r <= c && c < bw) ? Tb[r + c * ib] : 0.0;
     }
+    group_sync(gbar);
+    prof_mark(PH_MMA1);
+
     // ---- reduction: W^T = the group's 4 partials (+ the C1 window: identity part of V);
     // every warp reduces the accumulator positions of its own n-tile rg (a quarter of
     // the group's W^T) instead of all four warps summing all of it while loading
