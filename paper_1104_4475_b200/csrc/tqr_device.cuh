@@ -674,11 +674,12 @@ __device__ __forceinline__ void su_p1(const double (&acc)[kSlots][4], double (&w
 }
 // phase 3 on N slots: C^T += W2^T V^T (W2^T fragments wa0/wa1 per k-step; V already masked)
 template <int KIND, int N>
-__device__ __forceinline__ void su_p3(double (&acc)[kSlots][4], const double (&wa0)[8], const double (&wa1)[8],
-                                      const double *Vb, int rg, int ntile) {
+__device__ __forceinline__ void su_p3(double (&acc)[kSlots][4], const double *W2c, const double *Vb, int rg,
+                                      int ntile) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
+    const double wa0 = W2c[(4 * kk) * kLdw], wa1 = W2c[8 + (4 * kk) * kLdw];   // W2^T fragment of this k-step
     double bb[N > 0 ? N : 1];
 #pragma unroll
     for (int s = 0; s < N; ++s) {
@@ -686,7 +687,7 @@ __device__ __forceinline__ void su_p3(double (&acc)[kSlots][4], const double (&w
       bb[s] = Vb[j * 256 + (4 * ((TQR_EXP & 256) ? 0 : kk) + t) * 8 + g];
     }
 #pragma unroll
-    for (int s = 0; s < N; ++s) dmma(acc[s], wa0[kk], wa1[kk], bb[s]);
+    for (int s = 0; s < N; ++s) dmma(acc[s], wa0, wa1, bb[s]);
   }
 }
 
@@ -882,14 +883,8 @@ __device__ __forceinline__ void su_loop(const StripJob &J, const StripJob *JN, d
 
     // ---- phase 3: C^T += W2^T V^T on this warp's row tiles
     {
-      const double *W2 = smem + L.offW2;
-      double wa0[8], wa1[8];
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        wa0[kk] = W2[cg + (4 * kk + t) * kLdw];
-        wa1[kk] = W2[cg + 8 + (4 * kk + t) * kLdw];
-      }
-#define TQR_P3(N) su_p3<KIND, N>(acc, wa0, wa1, Vb, rg, ntile)
+      const double *W2c = smem + L.offW2 + cg + t * kLdw;
+#define TQR_P3(N) su_p3<KIND, N>(acc, W2c, Vb, rg, ntile)
       for (int rep = 0; rep < ((TQR_EXP & 64) ? 4 : 1); ++rep) {
         TQR_SLOT_SWITCH(nact, TQR_P3)
       }
